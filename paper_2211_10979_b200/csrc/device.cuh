@@ -1,0 +1,79 @@
+// device.cuh — data structures shared by the libsimplex kernels and the host engine.
+//
+// Layout of one slab in HBM:
+//   T        (m+1) x ld doubles, row-major, ld = roundup(w+1, 16) so every row starts on
+//            a 128-byte line; local column j < w is global column c0 + j, local column w
+//            is the (replicated) rhs "cv", columns w+1 .. ld-1 are zero
+//            padding (they stay exactly zero: prow_j = 0/p = 0 and fma(-a, 0, 0) = 0).
+//   col      m+1 (+2 pad) staged pivot column T[.][k]   (snapshot, read by the update)
+//   rownorm  ld   normalized pivot row T[r][.]/p          (written back one pivot later)
+//   price    nc   per-column-chunk argmin candidates of the NEW row 0 (fused pricing)
+//   rcand    ratio-test block candidates
+#pragma once
+#include <cstdint>
+
+namespace sx {
+
+constexpr int kRunning = -1;
+constexpr int kOptimal = 0;
+constexpr int kUnbounded = 2;
+constexpr int kIterLimit = 4;
+
+constexpr int kThreads = 256;              // threads per CTA for every kernel
+constexpr int kChunk = 2 * kThreads;       // max doubles per column chunk (one double2 / thread)
+
+constexpr uint32_t kErrNonFinite = 1u;
+constexpr uint32_t kErrNegRhs = 2u;
+
+// (value, index) argmin candidate; "none" = (+inf, INT64_MAX).  Compared
+// lexicographically, which equals the oracle's ascending strict-< scan when no NaN
+// is present.
+struct Cand {
+  double v;
+  long long idx;
+};
+
+// Device-resident loop state (one per slab).  Written only by the single "last
+// block" of k_select (and by the host between launches); read by every kernel.
+struct alignas(16) DevState {
+  long long it;        // pivots done
+  long long cap;       // iteration cap (reading c12)
+  long long stop_at;   // stop before pivot number stop_at (simplex_iterate)
+  double p;            // current pivot element T[r][k]
+  int status;          // kRunning / kOptimal / kUnbounded / kIterLimit
+  int go;              // 1: k_update must apply pivot (r, k, p)
+  int r;               // pivot row, 1-based
+  int k;               // entering column, global
+  int pend_r;          // row whose normalized values still sit in rownorm (-1: none)
+  unsigned int err;    // build/validation error bits
+  unsigned int ticket; // last-block ticket of k_select
+  unsigned int ticket2;
+};
+
+struct SlabView {
+  double* T;
+  long long ld;
+  int rows;            // m + 1
+  int w;               // local non-rhs columns; rhs is local column w
+  long long c0;        // global index of local column 0
+  int nc;              // column chunks (pricing / update)
+  int cw;              // chunk width in doubles (even, <= kChunk)
+  Cand* price;         // [nc]
+  double* col;         // [rows + 2]
+  double* rownorm;     // [ld]
+  Cand* rcand;         // [ratio-test blocks]
+  int* basis;          // [m]
+  int* trace_k;
+  int* trace_r;
+  long long trace_cap;
+  DevState* st;
+};
+
+// Where k_select takes the entering column from.
+struct XView {
+  int nparts;          // 1: own slab (single GPU);  >1: gathered per-rank candidates
+  const double* recv;  // nparts x stride: [v, k (int64 bits), col[0..m]]
+  long long stride;
+};
+
+}  // namespace sx

@@ -1,0 +1,619 @@
+// engine.cpp — libsimplex host engine and C ABI (include/libsimplex.h).
+//
+// One handle = one process's share of the tableau on one GPU:
+//   * column partition of the n+m non-rhs columns into P contiguous slabs of width
+//     floor((n+m)/P) or +1, remainder to the lowest parts, rhs replicated
+//     on every part;
+//   * P = nranks (one process per GPU, NCCL over NVLink) or virtual_ranks (several
+//     slabs on one GPU exchanging through device memory: same kernels, same data
+//     flow, used to test the multi-GPU path on one GPU);
+//   * the per-pivot loop runs entirely on the device inside
+//     captured CUDA-graph segments of S pivots; the host only looks at the status
+//     word once per segment, with two segments in flight so the GPU never waits.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/libsimplex.h"
+#include "device.cuh"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+simplex_err fail(simplex_err code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) return fail(e_ == cudaErrorMemoryAllocation ? SIMPLEX_E_OOM : SIMPLEX_E_CUDA, \
+                                       std::string(#x) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+#define NK(x)                                                                                   \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) return fail(SIMPLEX_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+#define RET(x)                                    \
+  do {                                            \
+    simplex_err e_ = (x);                         \
+    if (e_ != SIMPLEX_OK) return e_;              \
+  } while (0)
+
+long long roundup(long long a, long long b) { return (a + b - 1) / b * b; }
+
+struct Slab {
+  sx::SlabView v{};
+  long long units = 0;   // (chunk, row) work units of k_update
+  int upd_grid = 1;
+  size_t upd_smem = 0;
+  int sel_grid = 1;
+};
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev_);
+    if (prev_ != dev) cudaSetDevice(dev);
+    dev_ = dev;
+  }
+  ~DeviceGuard() {
+    if (prev_ != dev_) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = 0, dev_ = 0;
+};
+
+}  // namespace
+
+struct simplex_s {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;       // internal non-blocking stream (graphs are captured here)
+  cudaStream_t user_stream = nullptr;  // caller's stream (NULL = legacy default stream)
+  cudaEvent_t ev_user = nullptr, ev_loop0 = nullptr, ev_loop1 = nullptr;
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  long long m = 0, n = 0, W = 0;
+  int nranks = 1, rank = 0, nslabs = 1, nparts = 1;
+  simplex_options opt{};
+  long long cap = 0;
+  std::vector<Slab> slabs;
+  std::vector<void*> allocs;
+  // exchange
+  ncclComm_t comm = nullptr;
+  double* send = nullptr;
+  double* recv = nullptr;
+  long long xstride = 0;
+  // extraction scratch
+  double* d_x = nullptr;
+  double* d_y = nullptr;
+  double* d_obj = nullptr;
+  double* d_b = nullptr;
+  unsigned long long* d_hash = nullptr;
+  sx::DevState* h_state = nullptr;  // pinned, 3 slots: 2 segment mirrors + 1 sync copy
+  // graph segments
+  int S = 32;
+  bool graphs_ready = false;
+  cudaGraphExec_t seg[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> tev[2];
+  // host view of the loop
+  int status = SIMPLEX_RUNNING;
+  long long it = 0;
+  // stats
+  long long graph_launches = 0, kernel_launches = 0, upd_launches = 0;
+  double upd_ms = 0.0, loop_ms = 0.0;
+
+  template <class T>
+  simplex_err dalloc(T** p, size_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+    if (e != cudaSuccess)
+      return fail(SIMPLEX_E_OOM, std::string("cudaMalloc(") + std::to_string(count * sizeof(T)) +
+                                     " B): " + cudaGetErrorString(e));
+    allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return SIMPLEX_OK;
+  }
+
+  sx::XView xview() const {
+    sx::XView x{};
+    x.nparts = nparts;
+    x.recv = nparts > 1 ? recv : nullptr;
+    x.stride = xstride;
+    return x;
+  }
+
+  int kernels_per_pivot() const { return nslabs * (2 + (nparts > 1 ? 1 : 0)); }
+
+  simplex_err enter() {
+    // order our stream after whatever the caller queued on its stream (e.g. inputs)
+    CK(cudaEventRecord(ev_user, user_stream));
+    CK(cudaStreamWaitEvent(stream, ev_user, 0));
+    return SIMPLEX_OK;
+  }
+
+  simplex_err setup(long long m_, long long n_, const simplex_options* o);
+  simplex_err load(const double* A, const double* b, const double* c);
+  simplex_err build_graphs();
+  simplex_err enqueue_pivot(int slot, int t);
+  simplex_err run(long long max_pivots, long long* done);
+  simplex_err flush_all();
+  void release();
+};
+
+simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* o) {
+  m = m_;
+  n = n_;
+  W = n + m + 1;
+  opt = *o;
+  nranks = std::max(1, opt.nranks);
+  rank = opt.rank;
+  nslabs = std::max(1, opt.virtual_ranks);
+  if (rank < 0 || rank >= nranks) return fail(SIMPLEX_E_ARG, "rank out of range");
+  if (nslabs > 1 && nranks > 1) return fail(SIMPLEX_E_ARG, "virtual_ranks requires nranks == 1");
+  nparts = nranks * nslabs;
+  if (nparts > n + m) return fail(SIMPLEX_E_ARG, "more column parts than columns");
+  if (m + 1 > INT_MAX / 2 || n + m > INT_MAX / 2) return fail(SIMPLEX_E_ARG, "dimensions too large");
+  cap = opt.max_pivots > 0 ? opt.max_pivots : 20 * (m + n);
+  S = opt.segment_pivots > 0 ? opt.segment_pivots : 32;
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(SIMPLEX_E_CUDA, "no CUDA device (libsimplex has no CPU fallback)");
+  if (opt.device >= 0) {
+    if (opt.device >= ndev) return fail(SIMPLEX_E_ARG, "device ordinal out of range");
+    device = opt.device;
+  } else {
+    CK(cudaGetDevice(&device));
+  }
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  user_stream = static_cast<cudaStream_t>(opt.stream);
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming));
+  CK(cudaEventCreate(&ev_loop0));
+  CK(cudaEventCreate(&ev_loop1));
+  for (auto& e : ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&h_state), 3 * sizeof(sx::DevState), cudaHostAllocDefault));
+
+  // ---- column partition: part p = rank * nslabs + s
+  const long long total = n + m;
+  const long long base = total / nparts, rem = total % nparts;
+  auto part_off = [&](long long p) { return p * base + std::min(p, rem); };
+  slabs.resize(nslabs);
+  for (int s = 0; s < nslabs; ++s) {
+    const long long p = (long long)rank * nslabs + s;
+    Slab& sl = slabs[s];
+    sx::SlabView& v = sl.v;
+    v.c0 = part_off(p);
+    v.w = (int)(part_off(p + 1) - v.c0);
+    v.rows = (int)(m + 1);
+    v.ld = roundup(v.w + 1, 16);
+    v.nc = (int)((v.ld + sx::kChunk - 1) / sx::kChunk);
+    v.cw = (int)roundup((v.ld + v.nc - 1) / v.nc, 2);
+    sl.units = (long long)v.nc * v.rows;
+    sl.sel_grid = (int)std::min<long long>((v.rows + sx::kThreads - 1) / sx::kThreads, 2LL * sms);
+    // k_update grid: all SMs, several CTAs each; segments of >= 32 rows
+    long long g0 = std::max<long long>(1, std::min<long long>(sl.units / 32, 4LL * sms));
+    long long seg = std::min<long long>(v.rows, (sl.units + g0 - 1) / g0);
+    size_t smem = sx::update_smem_bytes(v.cw, seg);
+    if (smem > 200 * 1024) return fail(SIMPLEX_E_ARG, "update segment too large for shared memory");
+    CK(sx::update_configure(smem));
+    int occ = 1;
+    CK(sx::update_occupancy(&occ, smem));
+    long long g = std::min<long long>(g0, (long long)std::max(1, occ) * sms);
+    if (g < g0) {
+      seg = std::min<long long>(v.rows, (sl.units + g - 1) / g);
+      smem = sx::update_smem_bytes(v.cw, seg);
+      CK(sx::update_configure(smem));
+    }
+    sl.upd_grid = (int)g;
+    sl.upd_smem = smem;
+
+    RET(dalloc(&v.T, (size_t)v.rows * v.ld));
+    RET(dalloc(&v.price, v.nc));
+    RET(dalloc(&v.col, v.rows + 2));
+    RET(dalloc(&v.rownorm, v.ld));
+    RET(dalloc(&v.rcand, sl.sel_grid));
+    RET(dalloc(&v.basis, m));
+    v.trace_cap = opt.record_trace ? cap : 0;
+    RET(dalloc(&v.trace_k, std::max<long long>(v.trace_cap, 1)));
+    RET(dalloc(&v.trace_r, std::max<long long>(v.trace_cap, 1)));
+    RET(dalloc(&v.st, 1));
+  }
+  RET(dalloc(&d_x, n));
+  RET(dalloc(&d_y, m));
+  RET(dalloc(&d_obj, 1));
+  RET(dalloc(&d_b, m));
+  RET(dalloc(&d_hash, 1));
+
+  // ---- exchange buffers
+  xstride = roundup(m + 3, 2);
+  if (nparts > 1) {
+    RET(dalloc(&recv, (size_t)nparts * xstride));
+    if (nranks > 1) RET(dalloc(&send, xstride));
+  }
+  if (nranks > 1) {
+    if (!opt.nccl_id) return fail(SIMPLEX_E_ARG, "nranks > 1 needs nccl_id");
+    ncclUniqueId id;
+    std::memcpy(&id, opt.nccl_id, sizeof(id));
+    NK(ncclCommInitRank(&comm, nranks, id, rank));
+  }
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
+  if (!A || !b || !c) return fail(SIMPLEX_E_ARG, "NULL input pointer");
+  RET(enter());
+  CK(cudaMemcpyAsync(d_b, b, sizeof(double) * m, cudaMemcpyDefault, stream));
+  for (auto& sl : slabs) {
+    sx::SlabView& v = sl.v;
+    const long long ns = std::max<long long>(0, std::min<long long>(v.c0 + v.w, n) - v.c0);  // structural cols
+    if (ns > 0) {
+      // A's slab columns straight into rows 1..m (pitched copy), c's into row 0
+      CK(cudaMemcpy2DAsync(v.T + v.ld, sizeof(double) * v.ld, A + v.c0, sizeof(double) * n,
+                           sizeof(double) * ns, m, cudaMemcpyDefault, stream));
+      CK(cudaMemcpyAsync(v.T, c + v.c0, sizeof(double) * ns, cudaMemcpyDefault, stream));
+    }
+    CK(sx::launch_init_state(v, n, cap, stream));
+    CK(sx::launch_build(v, d_b, n, stream, sms));
+    CK(sx::launch_price0(v, opt.tol_opt, stream));
+  }
+  kernel_launches += 3 * nslabs;
+  // validation result
+  unsigned int err = 0;
+  for (int s = 0; s < nslabs; ++s) {
+    CK(cudaMemcpyAsync(&h_state[2], slabs[s].v.st, sizeof(sx::DevState), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    err |= h_state[2].err;
+  }
+  if (nranks > 1) {
+    // every rank must agree on the verdict (each checked only its own columns)
+    unsigned int* d_err = reinterpret_cast<unsigned int*>(d_hash);
+    CK(cudaMemcpyAsync(d_err, &err, sizeof(err), cudaMemcpyHostToDevice, stream));
+    NK(ncclAllReduce(d_err, d_err, 1, ncclUint32, ncclMax, comm, stream));
+    CK(cudaMemcpyAsync(&h_state[2].err, d_err, sizeof(err), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    err = h_state[2].err;
+  }
+  status = SIMPLEX_RUNNING;
+  it = 0;
+  if (err & sx::kErrNonFinite) return fail(SIMPLEX_E_NONFINITE, "A, b or c contains NaN or Inf");
+  if (err & sx::kErrNegRhs) return fail(SIMPLEX_E_NEG_RHS, "b has a negative entry: slack basis infeasible");
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_s::enqueue_pivot(int slot, int t) {
+  if (nparts > 1) {
+    if (nranks > 1) {
+      CK(sx::launch_pack(slabs[0].v, send, slabs[0].sel_grid, stream));
+      NK(ncclAllGather(send, recv, (size_t)xstride, ncclFloat64, comm, stream));
+    } else {
+      for (int s = 0; s < nslabs; ++s)
+        CK(sx::launch_pack(slabs[s].v, recv + (long long)s * xstride, slabs[s].sel_grid, stream));
+    }
+  }
+  const sx::XView x = xview();
+  for (auto& sl : slabs) CK(sx::launch_select(sl.v, x, opt.tol_piv, sl.sel_grid, stream));
+  if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
+  for (auto& sl : slabs) CK(sx::launch_update(sl.v, sl.units, opt.tol_opt, sl.upd_grid, sl.upd_smem, stream));
+  if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_s::build_graphs() {
+  if (graphs_ready) return SIMPLEX_OK;
+  for (int slot = 0; slot < 2; ++slot) {
+    if (opt.time_kernels) {
+      tev[slot].resize(2 * S);
+      for (auto& e : tev[slot]) CK(cudaEventCreate(&e));
+    }
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    simplex_err e = SIMPLEX_OK;
+    for (int t = 0; t < S && e == SIMPLEX_OK; ++t) e = enqueue_pivot(slot, t);
+    if (e == SIMPLEX_OK) {
+      cudaError_t ce = cudaMemcpyAsync(&h_state[slot], slabs[0].v.st, sizeof(sx::DevState),
+                                       cudaMemcpyDeviceToHost, stream);
+      if (ce != cudaSuccess) e = fail(SIMPLEX_E_CUDA, std::string("capture memcpy: ") + cudaGetErrorString(ce));
+    }
+    cudaError_t ce = cudaStreamEndCapture(stream, &g);
+    if (e != SIMPLEX_OK) {
+      if (g) cudaGraphDestroy(g);
+      return e;
+    }
+    if (ce != cudaSuccess) return fail(SIMPLEX_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&seg[slot], g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(SIMPLEX_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ce));
+  }
+  graphs_ready = true;
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_s::run(long long max_pivots, long long* done) {
+  const long long it0 = it;
+  if (done) *done = 0;
+  if (status != SIMPLEX_RUNNING) return SIMPLEX_OK;
+  RET(build_graphs());
+  RET(enter());
+  const long long stop_at = max_pivots > 0 ? it + max_pivots : LLONG_MAX;
+  for (auto& sl : slabs) CK(sx::launch_set_stop(sl.v.st, stop_at, stream));
+  kernel_launches += nslabs;
+  CK(cudaEventRecord(ev_loop0, stream));
+  long long launched = 0, completed = 0, seen = it;
+  bool stop = false;
+  for (;;) {
+    while (!stop && launched - completed < 2) {
+      const int slot = (int)(launched & 1);
+      CK(cudaGraphLaunch(seg[slot], stream));
+      CK(cudaEventRecord(ev_done[slot], stream));
+      ++launched;
+      ++graph_launches;
+      kernel_launches += (long long)S * kernels_per_pivot();
+    }
+    const int slot = (int)(completed & 1);
+    CK(cudaEventSynchronize(ev_done[slot]));
+    const sx::DevState hs = h_state[slot];
+    ++completed;
+    const long long piv = hs.it - seen;
+    if (opt.time_kernels) {
+      for (long long q = 0; q < piv && q < S; ++q) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, tev[slot][2 * q], tev[slot][2 * q + 1]));
+        upd_ms += ms;
+        ++upd_launches;
+      }
+    }
+    seen = hs.it;
+    status = hs.status;
+    it = hs.it;
+    if (hs.status != SIMPLEX_RUNNING || hs.it >= stop_at) stop = true;
+    if (stop && completed == launched) break;
+  }
+  CK(cudaEventRecord(ev_loop1, stream));
+  CK(cudaEventSynchronize(ev_loop1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ev_loop0, ev_loop1));
+  loop_ms += ms;
+  if (done) *done = it - it0;
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_s::flush_all() {
+  for (auto& sl : slabs) CK(sx::launch_flush(sl.v, stream));
+  kernel_launches += nslabs;
+  return SIMPLEX_OK;
+}
+
+void simplex_s::release() {
+  if (device >= 0) cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& g : seg)
+    if (g) cudaGraphExecDestroy(g);
+  for (auto& v : tev)
+    for (auto e : v) cudaEventDestroy(e);
+  if (comm) ncclCommDestroy(comm);
+  for (void* p : allocs) cudaFree(p);
+  allocs.clear();
+  if (h_state) cudaFreeHost(h_state);
+  for (auto e : ev_done)
+    if (e) cudaEventDestroy(e);
+  if (ev_user) cudaEventDestroy(ev_user);
+  if (ev_loop0) cudaEventDestroy(ev_loop0);
+  if (ev_loop1) cudaEventDestroy(ev_loop1);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+// ====================================================================== C ABI
+extern "C" {
+
+void simplex_default_options(simplex_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->struct_size = sizeof(simplex_options);
+  o->tol_opt = 1e-7;
+  o->tol_piv = 1e-10;
+  o->max_pivots = 0;
+  o->record_trace = 1;
+  o->device = -1;
+  o->nranks = 1;
+  o->rank = 0;
+  o->nccl_id = nullptr;
+  o->stream = nullptr;
+  o->virtual_ranks = 1;
+  o->segment_pivots = 0;
+  o->time_kernels = 0;
+}
+
+simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* A, const double* b,
+                           const double* c, const simplex_options* opt) {
+  g_err.clear();
+  if (!out) return fail(SIMPLEX_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (m < 1 || n < 1) return fail(SIMPLEX_E_ARG, "m and n must be >= 1");
+  if (!A || !b || !c) return fail(SIMPLEX_E_ARG, "NULL input pointer");
+  simplex_options o;
+  simplex_default_options(&o);
+  if (opt) {
+    if (opt->struct_size != sizeof(simplex_options)) return fail(SIMPLEX_E_ARG, "simplex_options.struct_size mismatch");
+    o = *opt;
+  }
+  if (!(o.tol_opt >= 0.0) || !(o.tol_piv >= 0.0)) return fail(SIMPLEX_E_ARG, "tolerances must be >= 0");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  simplex_t* h = new simplex_s();
+  simplex_err e = h->setup(m, n, &o);
+  if (e == SIMPLEX_OK) e = h->load(A, b, c);
+  cudaSetDevice(prev);
+  if (e != SIMPLEX_OK) {
+    std::string keep = g_err;
+    h->release();
+    delete h;
+    g_err = keep;
+    return e;
+  }
+  *out = h;
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_reset(simplex_t* h, const double* A, const double* b, const double* c) {
+  g_err.clear();
+  if (!h) return fail(SIMPLEX_E_ARG, "NULL handle");
+  DeviceGuard dg(h->device);
+  return h->load(A, b, c);
+}
+
+simplex_err simplex_iterate(simplex_t* h, int64_t max_pivots, int64_t* pivots_done, simplex_status* st) {
+  g_err.clear();
+  if (!h) return fail(SIMPLEX_E_ARG, "NULL handle");
+  DeviceGuard dg(h->device);
+  long long done = 0;
+  simplex_err e = h->run(max_pivots, &done);
+  if (pivots_done) *pivots_done = done;
+  if (st) *st = static_cast<simplex_status>(h->status);
+  return e;
+}
+
+simplex_err simplex_solve(simplex_t* h, simplex_status* st) { return simplex_iterate(h, 0, nullptr, st); }
+
+simplex_err simplex_get_solution(simplex_t* h, double* x, double* y, double* objective, int64_t* pivots,
+                                 simplex_status* st) {
+  g_err.clear();
+  if (!h) return fail(SIMPLEX_E_ARG, "NULL handle");
+  DeviceGuard dg(h->device);
+  RET(h->enter());
+  RET(h->flush_all());
+  CK(cudaMemsetAsync(h->d_x, 0, sizeof(double) * h->n, h->stream));
+  CK(cudaMemsetAsync(h->d_y, 0, sizeof(double) * h->m, h->stream));
+  for (int s = 0; s < h->nslabs; ++s)
+    CK(sx::launch_extract(h->slabs[s].v, h->n, h->d_x, h->d_y, s == 0 ? h->d_obj : nullptr, h->stream));
+  h->kernel_launches += h->nslabs;
+  if (h->nranks > 1) NK(ncclAllReduce(h->d_y, h->d_y, (size_t)h->m, ncclFloat64, ncclSum, h->comm, h->stream));
+  if (x) CK(cudaMemcpyAsync(x, h->d_x, sizeof(double) * h->n, cudaMemcpyDefault, h->stream));
+  if (y) CK(cudaMemcpyAsync(y, h->d_y, sizeof(double) * h->m, cudaMemcpyDefault, h->stream));
+  double obj = 0.0;
+  CK(cudaMemcpyAsync(&h->h_state[2].p, h->d_obj, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  obj = h->h_state[2].p;
+  if (objective) *objective = obj;
+  if (pivots) *pivots = h->it;
+  if (st) *st = static_cast<simplex_status>(h->status);
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_get_trace(simplex_t* h, int32_t* k, int32_t* r, int64_t cap, int64_t* len) {
+  g_err.clear();
+  if (!h) return fail(SIMPLEX_E_ARG, "NULL handle");
+  DeviceGuard dg(h->device);
+  const sx::SlabView& v = h->slabs[0].v;
+  const long long n = std::min<long long>(std::min<long long>(h->it, v.trace_cap), std::max<int64_t>(cap, 0));
+  if (n > 0) {
+    if (!k || !r) return fail(SIMPLEX_E_ARG, "NULL trace buffer");
+    CK(cudaMemcpyAsync(k, v.trace_k, sizeof(int32_t) * n, cudaMemcpyDefault, h->stream));
+    CK(cudaMemcpyAsync(r, v.trace_r, sizeof(int32_t) * n, cudaMemcpyDefault, h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  if (len) *len = n;
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_get_tableau(simplex_t* h, double* T_out, int64_t ld_out) {
+  g_err.clear();
+  if (!h || !T_out) return fail(SIMPLEX_E_ARG, "NULL argument");
+  DeviceGuard dg(h->device);
+  long long cols = 1;
+  for (auto& sl : h->slabs) cols += sl.v.w;
+  if (ld_out < cols) return fail(SIMPLEX_E_ARG, "ld_out smaller than the slab's logical columns");
+  RET(h->enter());
+  RET(h->flush_all());
+  const long long base = h->slabs[0].v.c0;
+  for (auto& sl : h->slabs) {
+    const sx::SlabView& v = sl.v;
+    CK(cudaMemcpy2DAsync(T_out + (v.c0 - base), sizeof(double) * ld_out, v.T, sizeof(double) * v.ld,
+                         sizeof(double) * v.w, v.rows, cudaMemcpyDefault, h->stream));
+  }
+  const sx::SlabView& v0 = h->slabs[0].v;
+  CK(cudaMemcpy2DAsync(T_out + (cols - 1), sizeof(double) * ld_out, v0.T + v0.w, sizeof(double) * v0.ld,
+                       sizeof(double), v0.rows, cudaMemcpyDefault, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_tableau_hash(simplex_t* h, uint64_t* hash) {
+  g_err.clear();
+  if (!h || !hash) return fail(SIMPLEX_E_ARG, "NULL argument");
+  DeviceGuard dg(h->device);
+  RET(h->enter());
+  CK(cudaMemsetAsync(h->d_hash, 0, sizeof(unsigned long long), h->stream));
+  for (int s = 0; s < h->nslabs; ++s)
+    CK(sx::launch_hash(h->slabs[s].v, h->W, (h->rank == 0 && s == 0) ? 1 : 0, h->d_hash, h->stream, h->sms));
+  h->kernel_launches += h->nslabs;
+  if (h->nranks > 1)
+    NK(ncclAllReduce(h->d_hash, h->d_hash, 1, ncclUint64, ncclSum, h->comm, h->stream));
+  unsigned long long v = 0;
+  CK(cudaMemcpyAsync(&h->h_state[2].it, h->d_hash, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  std::memcpy(&v, &h->h_state[2].it, sizeof(v));
+  *hash = v;
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_get_stats(simplex_t* h, simplex_stats* s) {
+  g_err.clear();
+  if (!h || !s) return fail(SIMPLEX_E_ARG, "NULL argument");
+  std::memset(s, 0, sizeof(*s));
+  s->pivots = h->it;
+  s->update_launches = h->upd_launches;
+  s->update_ms_total = h->upd_ms;
+  s->loop_ms_total = h->loop_ms;
+  s->graph_launches = h->graph_launches;
+  s->kernel_launches = h->kernel_launches;
+  long long cols = 1;
+  for (auto& sl : h->slabs) cols += sl.v.w;
+  s->local_rows = h->m + 1;
+  s->local_cols = cols;
+  s->local_ld = h->slabs[0].v.ld;
+  s->col_offset = h->slabs[0].v.c0;
+  s->bytes_per_pivot = 16LL * (h->m + 1) * cols;
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_destroy(simplex_t* h) {
+  if (!h) return SIMPLEX_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  h->release();
+  delete h;
+  cudaSetDevice(prev);
+  return SIMPLEX_OK;
+}
+
+const char* simplex_last_error(void) { return g_err.c_str(); }
+
+simplex_err simplex_nccl_unique_id(void* out128) {
+  g_err.clear();
+  if (!out128) return fail(SIMPLEX_E_ARG, "NULL output");
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  std::memcpy(out128, &id, sizeof(id));
+  return SIMPLEX_OK;
+}
+
+const char* simplex_version(void) { return "libsimplex 0.1.0 (sm_100a, dense full-tableau simplex)"; }
+
+}  // extern "C"
