@@ -7,7 +7,7 @@
 //            padding (they stay exactly zero: prow_j = 0/p = 0 and fma(-a, 0, 0) = 0).
 //   col      m+1 (+2 pad) staged pivot column T[.][k]   (snapshot, read by the update)
 //   rownorm  ld   normalized pivot row T[r][.]/p          (written back one pivot later)
-//   price    nc   per-column-chunk argmin candidates of the NEW row 0 (fused pricing)
+//   price    nslot argmin candidates of the NEW row 0 per warp slot of 64 columns (fused pricing)
 //   rcand    ratio-test block candidates
 #pragma once
 #include <cstdint>
@@ -20,7 +20,6 @@ constexpr int kUnbounded = 2;
 constexpr int kIterLimit = 4;
 
 constexpr int kThreads = 256;              // threads per CTA for every kernel
-constexpr int kChunk = 2 * kThreads;       // max doubles per column chunk (one double2 / thread)
 
 constexpr uint32_t kErrNonFinite = 1u;
 constexpr uint32_t kErrNegRhs = 2u;
@@ -56,9 +55,8 @@ struct SlabView {
   int rows;            // m + 1
   int w;               // local non-rhs columns; rhs is local column w
   long long c0;        // global index of local column 0
-  int nc;              // column chunks (pricing / update)
-  int cw;              // chunk width in doubles (even, <= kChunk)
-  Cand* price;         // [nc]
+  int nslot;           // pricing slots: warps of 32 double2 of row 0 = ceil(ld/64)
+  Cand* price;         // [nslot]
   double* col;         // [rows + 2]
   double* rownorm;     // [ld]
   Cand* rcand;         // [ratio-test blocks]

@@ -56,9 +56,8 @@ long long roundup(long long a, long long b) { return (a + b - 1) / b * b; }
 
 struct Slab {
   sx::SlabView v{};
-  long long units = 0;   // (chunk, row) work units of k_update
+  int q = 1;             // k_update: rows swept concurrently (threads / (ld/2))
   int upd_grid = 1;
-  size_t upd_smem = 0;
   int sel_grid = 1;
 };
 
@@ -202,29 +201,19 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
     v.w = (int)(part_off(p + 1) - v.c0);
     v.rows = (int)(m + 1);
     v.ld = roundup(v.w + 1, 16);
-    v.nc = (int)((v.ld + sx::kChunk - 1) / sx::kChunk);
-    v.cw = (int)roundup((v.ld + v.nc - 1) / v.nc, 2);
-    sl.units = (long long)v.nc * v.rows;
+    v.nslot = (int)((v.ld / 2 + 31) / 32);
     sl.sel_grid = (int)std::min<long long>((v.rows + sx::kThreads - 1) / sx::kThreads, 2LL * sms);
-    // k_update grid: all SMs, several CTAs each; segments of >= 32 rows
-    long long g0 = std::max<long long>(1, std::min<long long>(sl.units / 32, 4LL * sms));
-    long long seg = std::min<long long>(v.rows, (sl.units + g0 - 1) / g0);
-    size_t smem = sx::update_smem_bytes(v.cw, seg);
-    if (smem > 200 * 1024) return fail(SIMPLEX_E_ARG, "update segment too large for shared memory");
-    CK(sx::update_configure(smem));
+    // k_update: kUpdateCtasPerSm CTAs per SM; thread t owns column pair t mod (ld/2)
     int occ = 1;
-    CK(sx::update_occupancy(&occ, smem));
-    long long g = std::min<long long>(g0, (long long)std::max(1, occ) * sms);
-    if (g < g0) {
-      seg = std::min<long long>(v.rows, (sl.units + g - 1) / g);
-      smem = sx::update_smem_bytes(v.cw, seg);
-      CK(sx::update_configure(smem));
-    }
-    sl.upd_grid = (int)g;
-    sl.upd_smem = smem;
+    CK(sx::update_occupancy(&occ));
+    const long long half = v.ld / 2;
+    long long threads = (long long)std::min(occ, sx::kUpdateCtasPerSm) * sms * sx::kThreads;
+    threads = std::max(threads, roundup(half, sx::kThreads));
+    sl.q = (int)std::max(1LL, std::min<long long>(v.rows, threads / half));
+    sl.upd_grid = (int)((sl.q * half + sx::kThreads - 1) / sx::kThreads);
 
     RET(dalloc(&v.T, (size_t)v.rows * v.ld));
-    RET(dalloc(&v.price, v.nc));
+    RET(dalloc(&v.price, v.nslot));
     RET(dalloc(&v.col, v.rows + 2));
     RET(dalloc(&v.rownorm, v.ld));
     RET(dalloc(&v.rcand, sl.sel_grid));
@@ -309,7 +298,7 @@ simplex_err simplex_s::enqueue_pivot(int slot, int t) {
   const sx::XView x = xview();
   for (auto& sl : slabs) CK(sx::launch_select(sl.v, x, opt.tol_piv, sl.sel_grid, stream));
   if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
-  for (auto& sl : slabs) CK(sx::launch_update(sl.v, sl.units, opt.tol_opt, sl.upd_grid, sl.upd_smem, stream));
+  for (auto& sl : slabs) CK(sx::launch_update(sl.v, sl.q, opt.tol_opt, sl.upd_grid, stream));
   if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
   return SIMPLEX_OK;
 }

@@ -70,41 +70,6 @@ __device__ __forceinline__ Cand ldcg_cand(const Cand* p) {
   return c;
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// 1-D TMA (cp.async.bulk) global -> shared with mbarrier completion.
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_barrier_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
 // ------------------------------------------------------------------ a0: build
 // Called after the host copied A's slab columns into rows 1..m (cudaMemcpy2DAsync)
 // and c's slab columns into row 0.  Writes everything else of Table I and checks
@@ -150,8 +115,6 @@ __global__ void k_init_state(SlabView s, long long n, long long cap) {
   const int m = s.rows - 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
     s.basis[i] = (int)(n + i);                     // slack basis
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.rows + 2; i += gridDim.x * blockDim.x)
-    if (i >= s.rows) s.col[i] = 0.0;               // bulk-copy padding of col
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevState* st = s.st;
     st->it = 0;
@@ -170,20 +133,22 @@ __global__ void k_init_state(SlabView s, long long n, long long cap) {
 }
 
 // ------------------------------------------------------------------ a1: initial pricing
-// One CTA per column chunk: candidates j < w with T[0][j] < -tol_opt (reading c3).
+// Row 0 is split into warp slots of 32 double2 (64 columns); slot w holds the argmin of
+// T[0][j] over its columns j < w_local with T[0][j] < -tol_opt (reading c3).  k_update
+// rewrites the same slots for the new row 0 of every pivot.
 __global__ void __launch_bounds__(kThreads) k_price0(SlabView s, double tol_opt) {
-  const int c = blockIdx.x;
-  const long long j0 = (long long)c * s.cw;
-  const long long jn = min(j0 + s.cw, s.ld);
-  const long long j = j0 + 2 * threadIdx.x;
+  const long long half = s.ld >> 1;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if ((t & ~31LL) >= half) return;                 // warp-uniform
   Cand best = cand_none();
-  if (j < jn) {
+  if (t < half) {
+    const long long j = 2 * t;
     const double2 v = *reinterpret_cast<const double2*>(s.T + j);
     if (j < s.w && v.x < -tol_opt) best = Cand{v.x, s.c0 + j};
     if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, Cand{v.y, s.c0 + j + 1});
   }
-  best = block_min(best);
-  if (threadIdx.x == 0) s.price[c] = best;
+  best = warp_min(best);
+  if ((threadIdx.x & 31) == 0) s.price[t >> 5] = best;
 }
 
 // ------------------------------------------------------------------ multi-GPU: pack
@@ -191,7 +156,7 @@ __global__ void __launch_bounds__(kThreads) k_price0(SlabView s, double tol_opt)
 // deferred pivot row taken from rownorm) into send = [v, k bits, col[0..m]].
 __global__ void __launch_bounds__(kThreads) k_pack(SlabView s, double* __restrict__ send) {
   Cand best = cand_none();
-  for (int c = threadIdx.x; c < s.nc; c += blockDim.x) best = cand_min(best, s.price[c]);
+  for (int c = threadIdx.x; c < s.nslot; c += blockDim.x) best = cand_min(best, s.price[c]);
   best = block_min(best);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     send[0] = best.v;
@@ -234,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double
   if (active) {
     Cand best = cand_none();
     if (x.nparts == 1) {
-      for (int c = tid; c < s.nc; c += blockDim.x) best = cand_min(best, s.price[c]);
+      for (int c = tid; c < s.nslot; c += blockDim.x) best = cand_min(best, s.price[c]);
     } else {
       for (int q = tid; q < x.nparts; q += blockDim.x) {
         const double* h = x.recv + (long long)q * x.stride;
@@ -315,103 +280,78 @@ __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double
 }
 
 // ------------------------------------------------------------------ a4 (+a1): update
-// Static balanced schedule: the work is (column chunk, row) units in chunk-major order;
-// CTA b owns units [b*U/G, (b+1)*U/G).  Per segment (one chunk, a row range) the raw
-// pivot-row segment T[r][chunk] and col[rows] are staged into shared memory by 1-D TMA
-// (cp.async.bulk + mbarrier).  prow = T[r][j]/p lives in registers (one double2 per
-// thread); each row is streamed once with 128-bit loads/stores, URows rows in flight.
-// Row r is not written here: its normalized values go to rownorm and are written back
-// by the next k_select / k_flush (so every CTA can read the raw row r without a race).
+// Column-owner, row-strided schedule (measured best on B200, profiles/ubench_update_r01.txt):
+// thread t owns the double2 column pair jp = t mod (ld/2) and rows k0 = t div (ld/2),
+// k0+q, k0+2q, ... where q = (resident threads) div (ld/2).  At any moment all resident
+// threads sweep q consecutive rows, so the chip-wide access front is one contiguous
+// stretch of HBM (the same locality as a plain copy), every access is a coalesced
+// 128-bit load/store, and prow_j = T[r][j] / p is computed ONCE per thread into
+// registers.  URows rows are in flight per thread.
+// Row r is not written: its normalized values go to rownorm and are written back by the
+// next k_select / k_flush, so the q threads of a column can all read the raw row r.
+// Row 0 (the threads with k0 == 0) also produces the Step-1 candidates of the next pivot
+// per warp slot (fused pricing, PAPER.md:90 on the new objective row).
 template <int URows>
-__global__ void __launch_bounds__(kThreads) k_update(SlabView s, long long units, double tol_opt) {
+__global__ void __launch_bounds__(kThreads) k_update(SlabView s, int q, double tol_opt) {
   const DevState* st = s.st;
   if (!st->go) return;
   const int r = st->r;
   const double p = st->p;
-  extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) uint64_t bar;
-  const int tid = threadIdx.x;
-  const int rows = s.rows;
   const long long ld = s.ld;
-  double* srow = smem;                       // [cw]
-  double* scol = smem + ((s.cw + 1) & ~1);   // [segment rows + 2]
+  const long long half = ld >> 1;
+  const int rows = s.rows;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool act = t < (long long)q * half;
+  const long long jp = act ? t % half : 0;
+  const int k0 = act ? (int)(t / half) : rows;
+  const long long j = 2 * jp;
+  double* Tj = s.T + j;
 
-  long long u0 = units * blockIdx.x / gridDim.x;
-  const long long u1 = units * (blockIdx.x + 1) / gridDim.x;
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_barrier_init();
+  double2 pr = make_double2(0.0, 0.0);
+  if (act) {
+    const double2 raw = *reinterpret_cast<const double2*>(s.T + (long long)r * ld + j);
+    pr.x = __ddiv_rn(raw.x, p);
+    pr.y = __ddiv_rn(raw.y, p);
+    if (r % q == k0) *reinterpret_cast<double2*>(s.rownorm + j) = pr;
   }
-  __syncthreads();
-  uint32_t phase = 0;
-
-  while (u0 < u1) {
-    const int c = (int)(u0 / rows);
-    const int i0 = (int)(u0 - (long long)c * rows);
-    const int i1 = (int)min((long long)rows, i0 + (u1 - u0));
-    const long long j0 = (long long)c * s.cw;
-    const long long jn = min(j0 + s.cw, ld);
-    const int ia = i0 & ~1;
-    const int ib = (i1 + 1) & ~1;
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      const uint32_t brow = (uint32_t)((jn - j0) * sizeof(double));
-      const uint32_t bcol = (uint32_t)((ib - ia) * sizeof(double));
-      mbar_arrive_expect_tx(&bar, brow + bcol);
-      bulk_g2s(srow, s.T + (long long)r * ld + j0, brow, &bar);
-      bulk_g2s(scol, s.col + ia, bcol, &bar);
+  // first row of every thread (row 0 for k0 == 0 -> pricing of the next pivot)
+  Cand best = cand_none();
+  if (act) {
+    double2 v = *reinterpret_cast<const double2*>(Tj + (long long)k0 * ld);
+    const double a = -__ldg(s.col + k0);
+    v.x = __fma_rn(a, pr.x, v.x);
+    v.y = __fma_rn(a, pr.y, v.y);
+    if (k0 != r) *reinterpret_cast<double2*>(Tj + (long long)k0 * ld) = v;
+    if (k0 == 0) {
+      if (j < s.w && v.x < -tol_opt) best = Cand{v.x, s.c0 + j};
+      if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, Cand{v.y, s.c0 + j + 1});
     }
-    mbar_wait(&bar, phase);
-    phase ^= 1u;
-
-    const long long j = j0 + 2 * tid;
-    const bool act = j < jn;
-    double2 pr = make_double2(0.0, 0.0);
-    if (act) {
-      pr.x = __ddiv_rn(srow[2 * tid], p);
-      pr.y = __ddiv_rn(srow[2 * tid + 1], p);
-      if (r >= i0 && r < i1) *reinterpret_cast<double2*>(s.rownorm + j) = pr;
-    }
-    double* Tj = s.T + j;
-    int i = i0;
-    if (i == 0) {                            // row 0: update + Step 1 of the next pivot
-      Cand best = cand_none();
-      if (act) {
-        double2 v = *reinterpret_cast<const double2*>(Tj);
-        const double a = -scol[0 - ia];
-        v.x = __fma_rn(a, pr.x, v.x);
-        v.y = __fma_rn(a, pr.y, v.y);
-        *reinterpret_cast<double2*>(Tj) = v;
-        if (j < s.w && v.x < -tol_opt) best = Cand{v.x, s.c0 + j};
-        if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, Cand{v.y, s.c0 + j + 1});
-      }
-      best = block_min(best);
-      if (tid == 0) s.price[c] = best;
-      i = 1;
-    }
-    if (act) {
-      for (; i + URows <= i1; i += URows) {
-        double2 v[URows];
+  }
+  if ((t & ~31LL) < half) {                        // warp-uniform: warps holding row-0 lanes
+    best = warp_min(best);
+    if ((threadIdx.x & 31) == 0) s.price[t >> 5] = best;
+  }
+  if (!act) return;
+  int i = k0 + q;
+  for (; i + (URows - 1) * q < rows; i += URows * q) {
+    double2 v[URows];
 #pragma unroll
-        for (int u = 0; u < URows; ++u) v[u] = *reinterpret_cast<const double2*>(Tj + (long long)(i + u) * ld);
+    for (int u = 0; u < URows; ++u) v[u] = *reinterpret_cast<const double2*>(Tj + (long long)(i + u * q) * ld);
 #pragma unroll
-        for (int u = 0; u < URows; ++u) {
-          const double a = -scol[i + u - ia];
-          v[u].x = __fma_rn(a, pr.x, v[u].x);
-          v[u].y = __fma_rn(a, pr.y, v[u].y);
-          if (i + u != r) *reinterpret_cast<double2*>(Tj + (long long)(i + u) * ld) = v[u];
-        }
-      }
-      for (; i < i1; ++i) {
-        double2 v = *reinterpret_cast<const double2*>(Tj + (long long)i * ld);
-        const double a = -scol[i - ia];
-        v.x = __fma_rn(a, pr.x, v.x);
-        v.y = __fma_rn(a, pr.y, v.y);
-        if (i != r) *reinterpret_cast<double2*>(Tj + (long long)i * ld) = v;
-      }
+    for (int u = 0; u < URows; ++u) {
+      const int iu = i + u * q;
+      const double a = -__ldg(s.col + iu);
+      v[u].x = __fma_rn(a, pr.x, v[u].x);
+      v[u].y = __fma_rn(a, pr.y, v[u].y);
+      if (iu != r) *reinterpret_cast<double2*>(Tj + (long long)iu * ld) = v[u];
     }
-    u0 += i1 - i0;
-    __syncthreads();                         // smem reused by the next segment
+  }
+  for (; i < rows; i += q) {
+    double2 v = *reinterpret_cast<const double2*>(Tj + (long long)i * ld);
+    const double a = -__ldg(s.col + i);
+    v.x = __fma_rn(a, pr.x, v.x);
+    v.y = __fma_rn(a, pr.y, v.y);
+    if (i != r) *reinterpret_cast<double2*>(Tj + (long long)i * ld) = v;
   }
 }
 
@@ -498,7 +438,8 @@ cudaError_t launch_init_state(const SlabView& s, long long n, long long cap, cud
 }
 
 cudaError_t launch_price0(const SlabView& s, double tol_opt, cudaStream_t st) {
-  k_price0<<<s.nc, kThreads, 0, st>>>(s, tol_opt);
+  const long long half = s.ld >> 1;
+  k_price0<<<(int)((half + kThreads - 1) / kThreads), kThreads, 0, st>>>(s, tol_opt);
   SX_CHECK_LAUNCH();
 }
 
@@ -512,21 +453,12 @@ cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int
   SX_CHECK_LAUNCH();
 }
 
-size_t update_smem_bytes(int cw, long long max_seg_rows) {
-  return (size_t)(((cw + 1) & ~1) + max_seg_rows + 4) * sizeof(double);
+cudaError_t update_occupancy(int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_update<kUpdateRows>, kThreads, 0);
 }
 
-cudaError_t update_configure(size_t smem) {
-  return cudaFuncSetAttribute(k_update<kUpdateRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-cudaError_t update_occupancy(int* blocks_per_sm, size_t smem) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_update<kUpdateRows>, kThreads, smem);
-}
-
-cudaError_t launch_update(const SlabView& s, long long units, double tol_opt, int grid, size_t smem,
-                          cudaStream_t st) {
-  k_update<kUpdateRows><<<grid, kThreads, smem, st>>>(s, units, tol_opt);
+cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st) {
+  k_update<kUpdateRows><<<grid, kThreads, 0, st>>>(s, q, tol_opt);
   SX_CHECK_LAUNCH();
 }
 

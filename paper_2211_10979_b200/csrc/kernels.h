@@ -6,7 +6,8 @@
 
 namespace sx {
 
-constexpr int kUpdateRows = 8;   // rows in flight per thread in k_update
+constexpr int kUpdateRows = 4;   // rows in flight per thread in k_update (measured)
+constexpr int kUpdateCtasPerSm = 4;
 
 cudaError_t launch_set_stop(DevState* st, long long stop_at, cudaStream_t s);
 cudaError_t launch_build(const SlabView& s, const double* b, long long n, cudaStream_t st, int sms);
@@ -14,11 +15,8 @@ cudaError_t launch_init_state(const SlabView& s, long long n, long long cap, cud
 cudaError_t launch_price0(const SlabView& s, double tol_opt, cudaStream_t st);
 cudaError_t launch_pack(const SlabView& s, double* send, int grid, cudaStream_t st);
 cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int grid, cudaStream_t st);
-size_t update_smem_bytes(int cw, long long max_seg_rows);
-cudaError_t update_configure(size_t smem);
-cudaError_t update_occupancy(int* blocks_per_sm, size_t smem);
-cudaError_t launch_update(const SlabView& s, long long units, double tol_opt, int grid, size_t smem,
-                          cudaStream_t st);
+cudaError_t update_occupancy(int* blocks_per_sm);
+cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st);
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st);
 cudaError_t launch_extract(const SlabView& s, long long n, double* x, double* y, double* obj, cudaStream_t st);
 cudaError_t launch_hash(const SlabView& s, long long Wg, int include_rhs, unsigned long long* out,
