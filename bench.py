@@ -42,12 +42,32 @@ def parse():
     ap.add_argument("--impl", default="libsimplex", choices=["libsimplex", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
+    ap.add_argument("--roofline-pivots", type=int, default=4000)
     return ap.parse_args()
 
 
 def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
         int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def reduce_max(v, world, dev):
+    """Max of a per-rank scalar over all ranks (multi-GPU times are max over ranks)."""
+    if world <= 1:
+        return v
+    import torch
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(v, world, dev):
+    if world <= 1:
+        return v
+    import torch
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t)
+    return float(t.item())
 
 
 def load_peaks():
@@ -190,7 +210,7 @@ def main():
     dy = torch.empty(m, dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
 
-    solver = sx.Simplex(dA, db, dc, group=group, time_kernels=True)
+    solver = sx.Simplex(dA, db, dc, group=group)
     st = solver.stats()
     tableau_bytes = 8 * (m + 1) * (n + m + 1)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -252,17 +272,27 @@ def main():
     s1 = solver.stats()
     total_ms = sum(times)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = reduce_max(total_ms, world, dev)
     value = pivs / (total_ms / 1e3)
 
-    upd_launches = s1.update_launches - s0.update_launches
-    upd_ms = s1.update_ms_total - s0.update_ms_total
+    # ---- roofline pass: the same solve with CUDA events around every k_update launch
+    # (event-record nodes in the captured graph, on the stream the kernel runs on).  Kept
+    # out of the value steps because an event node between two pivot kernels disables the
+    # programmatic-dependent-launch edge the production loop uses.
+    prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True)
+    barrier()
+    window = min(piv, args.roofline_pivots)
+    prof.iterate(window)
+    barrier()
+    sp = prof.stats()
+    prof.close()
+    upd_launches = sp.update_launches
+    upd_ms = sp.update_ms_total
     avg_upd_s = upd_ms / 1e3 / max(1, upd_launches)
     achieved = st.bytes_per_pivot / avg_upd_s / 1e9
     peak, peak_src = load_peaks()
     loop_ms = s1.loop_ms_total - s0.loop_ms_total
+    prof_loop_ms = sp.loop_ms_total
 
     # ---- e2e: same metric through the C ABI with HOST buffers (pinned), copies inside
     Ah = torch.from_numpy(A).pin_memory()
@@ -279,15 +309,11 @@ def main():
     barrier()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = reduce_max(e2e_ms, world, dev)
     ns_local = max(0, min(st.col_offset + st.local_cols - 1, n) - st.col_offset)
     h2d = 8 * (m * ns_local + m + ns_local)
     if world > 1:
-        t = torch.tensor([h2d], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t)
-        h2d = int(t.item())
+        h2d = int(reduce_sum(h2d, world, dev))
     d2h = world * 8 * (n + m + 1)
 
     cpu = None
@@ -315,7 +341,8 @@ def main():
                          "bytes_per_launch": st.bytes_per_pivot,
                          "bytes_formula": "16*(m+1)*(local columns incl. rhs) per pivot",
                          "avg_launch_us": avg_upd_s * 1e6, "launches_timed": upd_launches,
-                         "update_share_of_loop": upd_ms / loop_ms if loop_ms > 0 else None,
+                         "timed_window": f"first {window} pivots of the same solve, events per launch",
+                         "update_share_of_loop": upd_ms / prof_loop_ms if prof_loop_ms > 0 else None,
                          "loop_gbs": st.bytes_per_pivot * pivs / (loop_ms / 1e3) / 1e9 if loop_ms > 0 else None},
             "cpu_baseline": cpu,
             "e2e": {"value": piv_e2e / (e2e_ms / 1e3), "unit": "pivots/s", "h2d_bytes_per_step": h2d,

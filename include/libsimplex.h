@@ -165,6 +165,14 @@ const char* simplex_last_error(void);
  * broadcasts the bytes to the other ranks, e.g. with torch.distributed). */
 simplex_err simplex_nccl_unique_id(void* out128);
 
+/* Column partition of the n+m non-rhs columns over nparts parts ("the
+ * columns of the simplex tableau are equivalently spread among all the resources";
+ * SPEC.md:156-164): contiguous ranges of width floor(total/nparts) or +1, the
+ * remainder going to the lowest parts.  Part p gets [*c0, *c0 + *width).  Pure host
+ * function (no GPU needed); the handle uses it for its slab.  ARG on bad input. */
+simplex_err simplex_partition(int64_t total_cols, int64_t nparts, int64_t part, int64_t* c0,
+                              int64_t* width);
+
 /* Library version string. */
 const char* simplex_version(void);
 

@@ -34,7 +34,7 @@ STATUS_NAME = {RUNNING: "RUNNING", OPTIMAL: "OPTIMAL", UNBOUNDED: "UNBOUNDED",
 EXPORTS = ["simplex_default_options", "simplex_create", "simplex_reset", "simplex_iterate",
            "simplex_solve", "simplex_get_solution", "simplex_get_trace", "simplex_get_tableau",
            "simplex_tableau_hash", "simplex_get_stats", "simplex_destroy", "simplex_last_error",
-           "simplex_nccl_unique_id", "simplex_version"]
+           "simplex_nccl_unique_id", "simplex_partition", "simplex_version"]
 
 
 class Options(C.Structure):
@@ -86,6 +86,7 @@ def lib():
         L.simplex_last_error.argtypes = []
         L.simplex_last_error.restype = C.c_char_p
         L.simplex_nccl_unique_id.argtypes = [vp]
+        L.simplex_partition.argtypes = [i64, i64, i64, pi64, pi64]
         L.simplex_version.argtypes = []
         L.simplex_version.restype = C.c_char_p
         for name in EXPORTS:   # simplex_err-returning entry points
@@ -110,6 +111,23 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().simplex_nccl_unique_id(buf))
     return buf.raw
+
+
+def partition(total_cols: int, nparts: int, part: int):
+    """(c0, width) of column part `part` (simplex_partition)."""
+    c0, w = C.c_int64(), C.c_int64()
+    _check(lib().simplex_partition(int(total_cols), int(nparts), int(part), C.byref(c0), C.byref(w)))
+    return c0.value, w.value
+
+
+def share_nccl_id(group) -> bytes:
+    """Rank 0 of the torch.distributed group draws a fresh ncclUniqueId; every rank
+    returns the same 128 bytes (broadcast over the group's own backend)."""
+    import torch.distributed as dist
+    obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0), group=group)
+    assert isinstance(obj[0], (bytes, bytearray)) and len(obj[0]) == 128
+    return bytes(obj[0])
 
 
 def version() -> str:
@@ -170,9 +188,7 @@ class Simplex:
             o.nranks = dist.get_world_size(group)
             o.rank = dist.get_rank(group)
             if o.nranks > 1:
-                obj = [nccl_unique_id() if o.rank == 0 else None]
-                dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0), group=group)
-                self._idbuf = C.create_string_buffer(obj[0], 128)
+                self._idbuf = C.create_string_buffer(share_nccl_id(group), 128)
                 o.nccl_id = C.cast(self._idbuf, C.c_void_p)
         self.m, self.n = m, n
         self.nranks, self.rank = o.nranks, o.rank
@@ -257,5 +273,6 @@ def _out_ptr(a, keep):
     return C.c_void_p(a.ctypes.data)
 
 
-__all__ = ["Simplex", "SimplexError", "lib", "default_options", "nccl_unique_id", "version",
+__all__ = ["Simplex", "SimplexError", "lib", "default_options", "nccl_unique_id", "share_nccl_id",
+           "partition", "version",
            "OPTIMAL", "UNBOUNDED", "ITERATION_LIMIT", "RUNNING", "STATUS_NAME", "EXPORTS"]

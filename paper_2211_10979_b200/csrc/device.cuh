@@ -69,8 +69,9 @@ struct SlabView {
 
 // Where k_select takes the entering column from.
 struct XView {
-  int nparts;          // 1: own slab (single GPU);  >1: gathered per-rank candidates
-  const double* recv;  // nparts x stride: [v, k (int64 bits), col[0..m]]
+  int nparts;          // parts (ranks x virtual slabs) the columns are split over
+  const double* recv;  // NULL: entering column read from the own slab (one part);
+                       // else nparts x stride gathered [v, k (int64 bits), col[0..m]]
   long long stride;
 };
 

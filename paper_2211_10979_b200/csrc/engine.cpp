@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -105,6 +106,8 @@ struct simplex_s {
   sx::DevState* h_state = nullptr;  // pinned, 3 slots: 2 segment mirrors + 1 sync copy
   // graph segments
   int S = 32;
+  bool pdl = true;                  // programmatic dependent launch between pivot kernels
+  bool force_nccl = false;          // test hook: 1-rank NCCL exchange on one GPU
   bool graphs_ready = false;
   cudaGraphExec_t seg[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> tev[2];
@@ -130,12 +133,15 @@ struct simplex_s {
   sx::XView xview() const {
     sx::XView x{};
     x.nparts = nparts;
-    x.recv = nparts > 1 ? recv : nullptr;
+    x.recv = gathered() ? recv : nullptr;
     x.stride = xstride;
     return x;
   }
 
-  int kernels_per_pivot() const { return nslabs * (2 + (nparts > 1 ? 1 : 0)); }
+  // the entering column travels through the exchange buffer (pack -> gather -> select)
+  bool gathered() const { return nparts > 1 || force_nccl; }
+  bool use_nccl() const { return nranks > 1 || force_nccl; }
+  int kernels_per_pivot() const { return nslabs * (2 + (gathered() ? 1 : 0)); }
 
   simplex_err enter() {
     // order our stream after whatever the caller queued on its stream (e.g. inputs)
@@ -168,6 +174,8 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
   if (m + 1 > INT_MAX / 2 || n + m > INT_MAX / 2) return fail(SIMPLEX_E_ARG, "dimensions too large");
   cap = opt.max_pivots > 0 ? opt.max_pivots : 20 * (m + n);
   S = opt.segment_pivots > 0 ? opt.segment_pivots : 32;
+  if (const char* e = std::getenv("SIMPLEX_NO_PDL")) pdl = !(e[0] == '1');
+  if (const char* e = std::getenv("SIMPLEX_FORCE_NCCL")) force_nccl = (e[0] == '1') && nranks == 1 && nslabs == 1;
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -189,16 +197,15 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
   CK(cudaHostAlloc(reinterpret_cast<void**>(&h_state), 3 * sizeof(sx::DevState), cudaHostAllocDefault));
 
   // ---- column partition: part p = rank * nslabs + s
-  const long long total = n + m;
-  const long long base = total / nparts, rem = total % nparts;
-  auto part_off = [&](long long p) { return p * base + std::min(p, rem); };
   slabs.resize(nslabs);
   for (int s = 0; s < nslabs; ++s) {
     const long long p = (long long)rank * nslabs + s;
     Slab& sl = slabs[s];
     sx::SlabView& v = sl.v;
-    v.c0 = part_off(p);
-    v.w = (int)(part_off(p + 1) - v.c0);
+    int64_t c0 = 0, w = 0;
+    RET(simplex_partition(n + m, nparts, p, &c0, &w));
+    v.c0 = c0;
+    v.w = (int)w;
     v.rows = (int)(m + 1);
     v.ld = roundup(v.w + 1, 16);
     v.nslot = (int)((v.ld / 2 + 31) / 32);
@@ -231,14 +238,18 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
 
   // ---- exchange buffers
   xstride = roundup(m + 3, 2);
-  if (nparts > 1) {
+  if (gathered()) {
     RET(dalloc(&recv, (size_t)nparts * xstride));
-    if (nranks > 1) RET(dalloc(&send, xstride));
+    if (use_nccl()) RET(dalloc(&send, xstride));
   }
-  if (nranks > 1) {
-    if (!opt.nccl_id) return fail(SIMPLEX_E_ARG, "nranks > 1 needs nccl_id");
+  if (use_nccl()) {
     ncclUniqueId id;
-    std::memcpy(&id, opt.nccl_id, sizeof(id));
+    if (nranks > 1) {
+      if (!opt.nccl_id) return fail(SIMPLEX_E_ARG, "nranks > 1 needs nccl_id");
+      std::memcpy(&id, opt.nccl_id, sizeof(id));
+    } else {
+      NK(ncclGetUniqueId(&id));
+    }
     NK(ncclCommInitRank(&comm, nranks, id, rank));
   }
   return SIMPLEX_OK;
@@ -269,7 +280,7 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
     CK(cudaStreamSynchronize(stream));
     err |= h_state[2].err;
   }
-  if (nranks > 1) {
+  if (use_nccl()) {
     // every rank must agree on the verdict (each checked only its own columns)
     unsigned int* d_err = reinterpret_cast<unsigned int*>(d_hash);
     CK(cudaMemcpyAsync(d_err, &err, sizeof(err), cudaMemcpyHostToDevice, stream));
@@ -286,19 +297,31 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
 }
 
 simplex_err simplex_s::enqueue_pivot(int slot, int t) {
-  if (nparts > 1) {
-    if (nranks > 1) {
-      CK(sx::launch_pack(slabs[0].v, send, slabs[0].sel_grid, stream));
+  // PDL (programmatic dependent launch) only between two of our kernels: not after an
+  // NCCL collective or an event-record node.
+  bool prev_is_ours = t > 0;   // previous node in the segment: k_update of the last pivot
+  if (gathered()) {
+    if (use_nccl()) {
+      CK(sx::launch_pack(slabs[0].v, send, slabs[0].sel_grid, stream, pdl && prev_is_ours && !opt.time_kernels));
       NK(ncclAllGather(send, recv, (size_t)xstride, ncclFloat64, comm, stream));
+      prev_is_ours = false;
     } else {
-      for (int s = 0; s < nslabs; ++s)
-        CK(sx::launch_pack(slabs[s].v, recv + (long long)s * xstride, slabs[s].sel_grid, stream));
+      for (int s = 0; s < nslabs; ++s) {
+        CK(sx::launch_pack(slabs[s].v, recv + (long long)s * xstride, slabs[s].sel_grid, stream,
+                           pdl && prev_is_ours && !opt.time_kernels));
+        prev_is_ours = true;
+      }
     }
   }
   const sx::XView x = xview();
-  for (auto& sl : slabs) CK(sx::launch_select(sl.v, x, opt.tol_piv, sl.sel_grid, stream));
+  for (auto& sl : slabs) {
+    CK(sx::launch_select(sl.v, x, opt.tol_piv, sl.sel_grid, stream, pdl && prev_is_ours && !opt.time_kernels));
+    prev_is_ours = true;
+  }
   if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
-  for (auto& sl : slabs) CK(sx::launch_update(sl.v, sl.q, opt.tol_opt, sl.upd_grid, stream));
+  for (auto& sl : slabs) {
+    CK(sx::launch_update(sl.v, sl.q, opt.tol_opt, sl.upd_grid, stream, pdl && !opt.time_kernels));
+  }
   if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
   return SIMPLEX_OK;
 }
@@ -491,7 +514,7 @@ simplex_err simplex_get_solution(simplex_t* h, double* x, double* y, double* obj
   for (int s = 0; s < h->nslabs; ++s)
     CK(sx::launch_extract(h->slabs[s].v, h->n, h->d_x, h->d_y, s == 0 ? h->d_obj : nullptr, h->stream));
   h->kernel_launches += h->nslabs;
-  if (h->nranks > 1) NK(ncclAllReduce(h->d_y, h->d_y, (size_t)h->m, ncclFloat64, ncclSum, h->comm, h->stream));
+  if (h->use_nccl()) NK(ncclAllReduce(h->d_y, h->d_y, (size_t)h->m, ncclFloat64, ncclSum, h->comm, h->stream));
   if (x) CK(cudaMemcpyAsync(x, h->d_x, sizeof(double) * h->n, cudaMemcpyDefault, h->stream));
   if (y) CK(cudaMemcpyAsync(y, h->d_y, sizeof(double) * h->m, cudaMemcpyDefault, h->stream));
   double obj = 0.0;
@@ -551,7 +574,7 @@ simplex_err simplex_tableau_hash(simplex_t* h, uint64_t* hash) {
   for (int s = 0; s < h->nslabs; ++s)
     CK(sx::launch_hash(h->slabs[s].v, h->W, (h->rank == 0 && s == 0) ? 1 : 0, h->d_hash, h->stream, h->sms));
   h->kernel_launches += h->nslabs;
-  if (h->nranks > 1)
+  if (h->use_nccl())
     NK(ncclAllReduce(h->d_hash, h->d_hash, 1, ncclUint64, ncclSum, h->comm, h->stream));
   unsigned long long v = 0;
   CK(cudaMemcpyAsync(&h->h_state[2].it, h->d_hash, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
@@ -600,6 +623,16 @@ simplex_err simplex_nccl_unique_id(void* out128) {
   NK(ncclGetUniqueId(&id));
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
   std::memcpy(out128, &id, sizeof(id));
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_partition(int64_t total_cols, int64_t nparts, int64_t part, int64_t* c0, int64_t* width) {
+  if (total_cols < 1 || nparts < 1 || part < 0 || part >= nparts || !c0 || !width)
+    return fail(SIMPLEX_E_ARG, "simplex_partition: bad arguments");
+  // widths floor(total/P) or +1, the remainder to the lowest parts
+  const int64_t base = total_cols / nparts, rem = total_cols % nparts;
+  *c0 = part * base + std::min(part, rem);
+  *width = base + (part < rem ? 1 : 0);
   return SIMPLEX_OK;
 }
 

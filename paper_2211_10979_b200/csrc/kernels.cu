@@ -63,6 +63,12 @@ __device__ __forceinline__ Cand block_min(Cand c) {
   return out;
 }
 
+// Programmatic dependent launch (PDL): let the next kernel of the pivot chain be
+// scheduled while this one runs, and wait for the previous one's results.  Both are
+// no-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ Cand ldcg_cand(const Cand* p) {
   Cand c;
   c.v = __ldcg(&p->v);
@@ -155,6 +161,8 @@ __global__ void __launch_bounds__(kThreads) k_price0(SlabView s, double tol_opt)
 // Fold this slab's pricing candidates into (v, k); write header + column k (with the
 // deferred pivot row taken from rownorm) into send = [v, k bits, col[0..m]].
 __global__ void __launch_bounds__(kThreads) k_pack(SlabView s, double* __restrict__ send) {
+  pdl_launch_dependents();
+  pdl_wait();
   Cand best = cand_none();
   for (int c = threadIdx.x; c < s.nslot; c += blockDim.x) best = cand_min(best, s.price[c]);
   best = block_min(best);
@@ -177,6 +185,8 @@ __global__ void __launch_bounds__(kThreads) k_pack(SlabView s, double* __restric
 // finish folds the Step-2 candidates into r and decides the status in the order of
 // reading c12: OPTIMAL (no k), UNBOUNDED (no r), ITERATION_LIMIT (it == cap), pivot.
 __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double tol_piv) {
+  pdl_launch_dependents();
+  pdl_wait();
   DevState* st = s.st;
   __shared__ int sh_last;
   const int tid = threadIdx.x;
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double
   const double* xcol = nullptr;
   if (active) {
     Cand best = cand_none();
-    if (x.nparts == 1) {
+    if (x.recv == nullptr) {
       for (int c = tid; c < s.nslot; c += blockDim.x) best = cand_min(best, s.price[c]);
     } else {
       for (int q = tid; q < x.nparts; q += blockDim.x) {
@@ -209,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double
     best = block_min(best);
     if (best.idx != LLONG_MAX) {
       k = best.idx;
-      if (x.nparts > 1) {
+      if (x.recv != nullptr) {
         for (int q = 0; q < x.nparts; ++q) {      // owner = the part that sent (v, k)
           const double* h = x.recv + (long long)q * x.stride;
           if (__double_as_longlong(h[1]) == k) { xcol = h + 2; break; }
@@ -293,6 +303,8 @@ __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double
 // per warp slot (fused pricing, PAPER.md:90 on the new objective row).
 template <int URows>
 __global__ void __launch_bounds__(kThreads) k_update(SlabView s, int q, double tol_opt) {
+  pdl_launch_dependents();
+  pdl_wait();
   const DevState* st = s.st;
   if (!st->go) return;
   const int r = st->r;
@@ -443,23 +455,35 @@ cudaError_t launch_price0(const SlabView& s, double tol_opt, cudaStream_t st) {
   SX_CHECK_LAUNCH();
 }
 
-cudaError_t launch_pack(const SlabView& s, double* send, int grid, cudaStream_t st) {
-  k_pack<<<grid, kThreads, 0, st>>>(s, send);
-  SX_CHECK_LAUNCH();
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex(void (*kern)(KArgs...), int grid, int block, cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int grid, cudaStream_t st) {
-  k_select<<<grid, kThreads, 0, st>>>(s, x, tol_piv);
-  SX_CHECK_LAUNCH();
+cudaError_t launch_pack(const SlabView& s, double* send, int grid, cudaStream_t st, bool pdl) {
+  return launch_ex(k_pack, grid, kThreads, st, pdl, s, send);
+}
+
+cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int grid, cudaStream_t st, bool pdl) {
+  return launch_ex(k_select, grid, kThreads, st, pdl, s, x, tol_piv);
 }
 
 cudaError_t update_occupancy(int* blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_update<kUpdateRows>, kThreads, 0);
 }
 
-cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st) {
-  k_update<kUpdateRows><<<grid, kThreads, 0, st>>>(s, q, tol_opt);
-  SX_CHECK_LAUNCH();
+cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st, bool pdl) {
+  return launch_ex(k_update<kUpdateRows>, grid, kThreads, st, pdl, s, q, tol_opt);
 }
 
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st) {

@@ -13,10 +13,11 @@ cudaError_t launch_set_stop(DevState* st, long long stop_at, cudaStream_t s);
 cudaError_t launch_build(const SlabView& s, const double* b, long long n, cudaStream_t st, int sms);
 cudaError_t launch_init_state(const SlabView& s, long long n, long long cap, cudaStream_t st);
 cudaError_t launch_price0(const SlabView& s, double tol_opt, cudaStream_t st);
-cudaError_t launch_pack(const SlabView& s, double* send, int grid, cudaStream_t st);
-cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int grid, cudaStream_t st);
+cudaError_t launch_pack(const SlabView& s, double* send, int grid, cudaStream_t st, bool pdl);
+cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int grid, cudaStream_t st,
+                          bool pdl);
 cudaError_t update_occupancy(int* blocks_per_sm);
-cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st);
+cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st, bool pdl);
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st);
 cudaError_t launch_extract(const SlabView& s, long long n, double* x, double* y, double* obj, cudaStream_t st);
 cudaError_t launch_hash(const SlabView& s, long long Wg, int include_rhs, unsigned long long* out,

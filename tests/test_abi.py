@@ -1,0 +1,132 @@
+"""The C-ABI boundary, on CPU (-m "not gpu"): libsimplex.so loads, exports every symbol
+include/libsimplex.h declares, the ctypes mirrors match the C struct layouts, host-only
+entry points work, and GPU entry points fail loudly (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2211_10979_b200 as sx
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "libsimplex.h")
+
+
+def header_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(simplex_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_declares_the_survey_boundary():
+    f = header_functions()
+    for name in ("simplex_create", "simplex_solve", "simplex_iterate", "simplex_get_solution",
+                 "simplex_destroy"):                      # BASELINE.json north_star (1)
+        assert name in f
+
+
+def test_every_declared_symbol_is_exported():
+    lib = sx.lib()
+    declared = header_functions()
+    assert sorted(sx.EXPORTS) == declared
+    out = subprocess.run(["nm", "-D", "--defined-only", sx.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (simplex_\w+)", out))
+    for name in declared:
+        assert name in exported, name
+        assert getattr(lib, name) is not None
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", sx.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+@pytest.fixture(scope="module")
+def c_sizes(tmp_path_factory):
+    d = tmp_path_factory.mktemp("abi")
+    src = d / "sizes.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "libsimplex.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu\\n", sizeof(simplex_options), sizeof(simplex_stats),'
+                   ' offsetof(simplex_options, stream), offsetof(simplex_stats, bytes_per_pivot));return 0;}\n')
+    exe = d / "sizes"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    return [int(v) for v in subprocess.check_output([str(exe)]).split()]
+
+
+def test_struct_layouts_match_header(c_sizes):
+    import ctypes as C
+    so, ss, off_stream, off_bpp = c_sizes
+    assert C.sizeof(sx.Options) == so
+    assert C.sizeof(sx.Stats) == ss
+    assert sx.Options.stream.offset == off_stream
+    assert sx.Stats.bytes_per_pivot.offset == off_bpp
+    o = sx.default_options()
+    assert o.struct_size == so
+    assert (o.tol_opt, o.tol_piv, o.max_pivots, o.record_trace, o.nranks, o.virtual_ranks) == \
+        (1e-7, 1e-10, 0, 1, 1, 1)
+
+
+def test_partition_largest_remainder():
+    # SPEC.md:162 (10 columns, equal weights, 2 lanes -> 5, 5) and the remainder-to-lowest rule
+    assert [sx.partition(10, 2, p) for p in range(2)] == [(0, 5), (5, 5)]
+    assert [sx.partition(7, 2, p)[1] for p in range(2)] == [4, 3]
+    for total in (1, 7, 128, 16000, 60000):
+        for P in (1, 2, 3, 4, 8):
+            if P > total:
+                continue
+            parts = [sx.partition(total, P, p) for p in range(P)]
+            assert parts[0][0] == 0 and sum(w for _, w in parts) == total
+            assert all(parts[i][0] + parts[i][1] == parts[i + 1][0] for i in range(P - 1))
+            assert max(w for _, w in parts) - min(w for _, w in parts) <= 1
+            assert [w for _, w in parts] == sorted([w for _, w in parts], reverse=True)
+    with pytest.raises(sx.SimplexError) as e:
+        sx.partition(10, 0, 0)
+    assert e.value.code == sx.E_ARG
+
+
+def test_nccl_unique_id_is_host_only():
+    a, b = sx.nccl_unique_id(), sx.nccl_unique_id()
+    assert len(a) == 128 and a != b
+
+
+def test_argument_errors_before_any_device_work():
+    A, b, c = np.ones((2, 2)), np.ones(2), np.ones(2)
+    with pytest.raises(sx.SimplexError) as e:
+        sx.Simplex(np.ones((0, 2)), np.ones(0), np.ones(2))
+    assert e.value.code == sx.E_ARG
+    import ctypes as C
+    h = C.c_void_p()
+    assert sx.lib().simplex_create(C.byref(h), 2, 2, None, None, None, None) == sx.E_ARG
+    assert sx.lib().simplex_destroy(None) == sx.OK
+    bad = sx.default_options()
+    bad.struct_size = 7
+    assert sx.lib().simplex_create(C.byref(h), 2, 2, A.ctypes.data, b.ctypes.data, c.ctypes.data,
+                                   C.byref(bad)) == sx.E_ARG
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(sx.SimplexError) as e:
+        sx.Simplex(np.ones((2, 2)), np.ones(2), np.ones(2))
+    assert e.value.code == sx.E_CUDA
+    assert "no CPU fallback" in str(e.value)
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2211_10979_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "simplex_oracle" not in text and "liboracle" not in text, f
+    oracle_src = open(os.path.join(ROOT, "oracle", "simplex_oracle.c")).read()
+    includes = re.findall(r"#include\s*[<\"]([^>\"]+)[>\"]", oracle_src)
+    assert includes and all(h in ("math.h", "stdint.h", "stdlib.h", "string.h") for h in includes)
+    oracle_py = open(os.path.join(ROOT, "oracle", "__init__.py")).read()
+    assert not re.search(r"^\s*(import|from)\s+paper_2211_10979_b200", oracle_py, flags=re.M)

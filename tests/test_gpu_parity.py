@@ -216,3 +216,34 @@ def test_golden_full_size(sx, key):
     assert h == int(g["tableau_hash"])
     cert = oracle.certificate(A, b, c, x, y)
     assert not cert.violations, cert.violations
+
+
+def test_nccl_exchange_path_one_rank(sx, monkeypatch):
+    """The multi-GPU exchange (k_pack -> ncclAllGather captured in the CUDA graph ->
+    k_select from the gathered buffer) run through a real 1-rank NCCL communicator."""
+    A, b, c = lpgen.dense_lp(150, 230, 21)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    monkeypatch.setenv("SIMPLEX_FORCE_NCCL", "1")
+    g = gpu_solve(sx, A, b, c)
+    assert_same(g, o)
+
+
+def test_wide_prefix_20000x40000(sx):
+    """BASELINE config 5 (~9.6 GB tableau): the first 32 pivots, row 0, rhs column and the
+    whole-tableau digest against the oracle's prefix run (tests/golden/*_p32.npz)."""
+    path = os.path.join(GOLDEN_DIR, "dense_20000x40000_s1_p32.npz")
+    g = np.load(path)
+    A, b, c = lpgen.dense_lp(20000, 40000, 1)
+    with sx.Simplex(A, b, c) as s:
+        done, st = s.iterate(32)
+        assert done == 32 and st == sx.RUNNING
+        k, r = s.trace()
+        h = s.tableau_hash()
+        x, y, obj, piv, _ = s.solution()
+    assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+    assert obj == float(g["objective"])
+    assert np.array_equal(y, g["y"])
+    xs = np.zeros(40000)
+    xs[g["x_idx"]] = g["x_val"]
+    assert np.array_equal(x, xs)
+    assert h == int(g["tableau_hash"])
