@@ -43,12 +43,24 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     ap.add_argument("--roofline-pivots", type=int, default=4000)
+    ap.add_argument("--lookahead", type=int, default=0,
+                    help="pivots per tableau pass (0: library default = 16 on one column part, 1 with "
+                         "N > 1; 1: one pass per pivot; 2..16: rank-s look-ahead)")
+    ap.add_argument("--single-pass-pivots", type=int, default=1000,
+                    help="pivots of the one-pivot-per-pass k_update roofline window (0: skip)")
     return ap.parse_args()
 
 
 def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
         int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def solver_look(lookahead, world):
+    """Pivots per tableau pass the library uses (mirrors simplex_options.lookahead = 0)."""
+    if lookahead > 0:
+        return lookahead
+    return 16 if world == 1 else 1
 
 
 def reduce_max(v, world, dev):
@@ -210,7 +222,7 @@ def main():
     dy = torch.empty(m, dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
 
-    solver = sx.Simplex(dA, db, dc, group=group)
+    solver = sx.Simplex(dA, db, dc, group=group, lookahead=args.lookahead)
     st = solver.stats()
     tableau_bytes = 8 * (m + 1) * (n + m + 1)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -279,7 +291,7 @@ def main():
     # (event-record nodes in the captured graph, on the stream the kernel runs on).  Kept
     # out of the value steps because an event node between two pivot kernels disables the
     # programmatic-dependent-launch edge the production loop uses.
-    prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True)
+    prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead)
     barrier()
     window = min(piv, args.roofline_pivots)
     prof.iterate(window)
@@ -293,6 +305,22 @@ def main():
     peak, peak_src = load_peaks()
     loop_ms = s1.loop_ms_total - s0.loop_ms_total
     prof_loop_ms = sp.loop_ms_total
+    look = solver_look(args.lookahead, world)
+
+    # ---- the one-pivot-per-pass kernel (k_update) measured the same way, for reference
+    single = None
+    if look > 1 and args.single_pass_pivots > 0:
+        p1 = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=1)
+        barrier()
+        p1.iterate(min(piv, args.single_pass_pivots))
+        barrier()
+        s1p = p1.stats()
+        p1.close()
+        a1 = s1p.update_ms_total / 1e3 / max(1, s1p.update_launches)
+        single = {"kernel": "k_update (one pivot per pass)", "avg_launch_us": a1 * 1e6,
+                  "achieved": st.bytes_per_pivot / a1 / 1e9, "peak": peak, "unit": "GB/s",
+                  "frac": st.bytes_per_pivot / a1 / 1e9 / peak, "launches_timed": s1p.update_launches,
+                  "traffic": ncu_traffic(args.workload, world)}
 
     # ---- e2e: same metric through the C ABI with HOST buffers (pinned), copies inside
     Ah = torch.from_numpy(A).pin_memory()
@@ -330,12 +358,16 @@ def main():
                     "SPEC.md:365-380 recipe)",
             "config": {"workload": f"dense random LP m={m} n={n} FP64 seed {args.seed}, slack basis, Dantzig "
                                    "+ lowest-index ties", "m": m, "n": n, "pivots_per_solve": piv,
+                       "pivots_per_tableau_pass": look,
                        "time_to_solve_ms": total_ms / args.steps,
                        "parallelism": f"column slabs x{world}" + (" (NCCL allgather/pivot)" if world > 1 else ""),
                        "l2": ("tableau %.2f GB > L2 %d MB: inputs larger than L2" % (tableau_bytes / 1e9, l2 >> 20))
                        if flush is None else "L2 flushed (write 2xL2) before every timed step",
                        "step": "reset (build Table I from device-resident A,b,c) + solve + extract"},
-            "roofline": {"bound": "hbm", "kernel": "k_update (fused row-scale + rank-1 update)",
+            "roofline": {"bound": "hbm",
+                         "kernel": (f"k_update_s (rank-{look} look-ahead pass: {look} pivots per tableau "
+                                    "stream, TMA-pipelined)") if look > 1 else
+                                   "k_update (fused row-scale + rank-1 update)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "peak_source": peak_src, "traffic": ncu_traffic(args.workload, world),
                          "bytes_per_launch": st.bytes_per_pivot,
@@ -343,7 +375,10 @@ def main():
                          "avg_launch_us": avg_upd_s * 1e6, "launches_timed": upd_launches,
                          "timed_window": f"first {window} pivots of the same solve, events per launch",
                          "update_share_of_loop": upd_ms / prof_loop_ms if prof_loop_ms > 0 else None,
-                         "loop_gbs": st.bytes_per_pivot * pivs / (loop_ms / 1e3) / 1e9 if loop_ms > 0 else None},
+                         "pivots_per_launch": look,
+                         "effective_gbs_per_pivot": st.bytes_per_pivot * pivs / (loop_ms / 1e3) / 1e9
+                         if loop_ms > 0 else None,
+                         "single_pass": single},
             "cpu_baseline": cpu,
             "e2e": {"value": piv_e2e / (e2e_ms / 1e3), "unit": "pivots/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms": e2e_ms,

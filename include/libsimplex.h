@@ -27,8 +27,8 @@
  *  - Solver OUTCOMES (optimal, unbounded, iteration limit) are simplex_status
  *    values, never errors.
  *  - Pointers to problem data and results may be HOST or DEVICE memory of the
- *    handle's GPU; the library detects which (cudaPointerGetAttributes) and
- *    copies accordingly.  Inputs are copied during the call; the caller keeps
+ *    handle's GPU; the library copies with cudaMemcpyDefault (unified virtual
+ *    addressing tells the runtime which).  Inputs are copied during the call; the caller keeps
  *    ownership and may free them on return.  Outputs go to caller buffers.
  *  - A handle owns all its device memory, streams, CUDA graphs and its NCCL
  *    communicator.  It is not thread-safe: one host thread per handle.
@@ -88,7 +88,11 @@ typedef struct {
     int32_t  segment_pivots;/* pivots per captured CUDA-graph segment (<= 0: automatic)    */
     int32_t  time_kernels;  /* 1: record CUDA events around every pivot-update launch
                                (see simplex_get_stats)                                     */
-    int32_t  reserved;
+    int32_t  lookahead;     /* pivots applied per pass over the tableau: 1 = one pivot per pass;
+                               2..16 = rank-s look-ahead blocks (select s pivots ahead from
+                               chained corrections, then ONE pass applies all s — bitwise
+                               identical to s single pivots; one column part only);
+                               0 (default) = 16 on one column part, else 1                 */
 } simplex_options;
 
 typedef struct {

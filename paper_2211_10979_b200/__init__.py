@@ -42,7 +42,7 @@ class Options(C.Structure):
                 ("max_pivots", C.c_int64), ("record_trace", C.c_int32), ("device", C.c_int32),
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_void_p),
                 ("stream", C.c_void_p), ("virtual_ranks", C.c_int32), ("segment_pivots", C.c_int32),
-                ("time_kernels", C.c_int32), ("reserved", C.c_int32)]
+                ("time_kernels", C.c_int32), ("lookahead", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -170,7 +170,7 @@ class Simplex:
 
     def __init__(self, A, b, c, *, tol_opt=1e-7, tol_piv=1e-10, max_pivots=0, record_trace=True,
                  device=None, group=None, virtual_ranks=1, segment_pivots=0, time_kernels=False,
-                 stream=None):
+                 lookahead=0, stream=None):
         L = lib()
         m, n = (int(A.shape[0]), int(A.shape[1]))
         o = default_options()
@@ -180,6 +180,7 @@ class Simplex:
         o.virtual_ranks = int(virtual_ranks)
         o.segment_pivots = int(segment_pivots)
         o.time_kernels = 1 if time_kernels else 0
+        o.lookahead = int(lookahead)
         s = stream if stream is not None else _current_stream()
         o.stream = s if s else None
         self._idbuf = None

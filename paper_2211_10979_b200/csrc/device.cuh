@@ -20,6 +20,8 @@ constexpr int kUnbounded = 2;
 constexpr int kIterLimit = 4;
 
 constexpr int kThreads = 256;              // threads per CTA for every kernel
+constexpr int kMaxLook = 16;               // max pivots per look-ahead block (rank-s update)
+constexpr int kLookThreads = 512;          // threads per CTA of the look-ahead selection (1 cluster)
 
 constexpr uint32_t kErrNonFinite = 1u;
 constexpr uint32_t kErrNegRhs = 2u;
@@ -47,6 +49,8 @@ struct alignas(16) DevState {
   unsigned int err;    // build/validation error bits
   unsigned int ticket; // last-block ticket of k_select
   unsigned int ticket2;
+  int s_eff;           // look-ahead: pivots selected for the pending rank-s pass
+  int rs[kMaxLook];    // look-ahead: their pivot rows, in order
 };
 
 struct SlabView {
@@ -65,6 +69,12 @@ struct SlabView {
   int* trace_r;
   long long trace_cap;
   DevState* st;
+  // rank-s look-ahead (NEXT #1); NULL when the handle runs 1 pivot/pass
+  double* colS;        // [rows][kMaxLook]  pivot columns T^t[.][k_t], t-minor
+  double* prowS;       // [kMaxLook][ld]    normalized pivot rows T^t[r_t][.] / p_t
+  double* R0;          // [ld]              current objective row during selection
+  double* RHS;         // [rows]            current rhs column during selection
+  Cand* pcand;         // [look-ahead CTAs] Step-1 candidates per CTA
 };
 
 // Where k_select takes the entering column from.

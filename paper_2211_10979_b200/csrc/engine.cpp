@@ -60,6 +60,8 @@ struct Slab {
   int q = 1;             // k_update: rows swept concurrently (threads / (ld/2))
   int upd_grid = 1;
   int sel_grid = 1;
+  int look_grid = 0;     // look-ahead selection: CTAs of its single thread-block cluster
+  int nc = 0, cw = 0, Gr = 0;   // rank-s pass: column chunks, chunk width, row groups
 };
 
 class DeviceGuard {
@@ -105,7 +107,8 @@ struct simplex_s {
   unsigned long long* d_hash = nullptr;
   sx::DevState* h_state = nullptr;  // pinned, 3 slots: 2 segment mirrors + 1 sync copy
   // graph segments
-  int S = 32;
+  int S = 32;                       // pivots per captured graph segment
+  int look = 1;                     // pivots per tableau pass (>1: rank-s look-ahead)
   bool pdl = true;                  // programmatic dependent launch between pivot kernels
   bool force_nccl = false;          // test hook: 1-rank NCCL exchange on one GPU
   bool graphs_ready = false;
@@ -142,6 +145,8 @@ struct simplex_s {
   bool gathered() const { return nparts > 1 || force_nccl; }
   bool use_nccl() const { return nranks > 1 || force_nccl; }
   int kernels_per_pivot() const { return nslabs * (2 + (gathered() ? 1 : 0)); }
+  int steps_per_segment() const { return look > 1 ? std::max(1, S / look) : S; }   // graph nodes
+  int kernels_per_segment() const { return look > 1 ? 2 * steps_per_segment() : S * kernels_per_pivot(); }
 
   simplex_err enter() {
     // order our stream after whatever the caller queued on its stream (e.g. inputs)
@@ -176,6 +181,11 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
   S = opt.segment_pivots > 0 ? opt.segment_pivots : 32;
   if (const char* e = std::getenv("SIMPLEX_NO_PDL")) pdl = !(e[0] == '1');
   if (const char* e = std::getenv("SIMPLEX_FORCE_NCCL")) force_nccl = (e[0] == '1') && nranks == 1 && nslabs == 1;
+  // 0 = automatic: rank-16 look-ahead on one column part, one pivot per pass otherwise
+  look = opt.lookahead > 0 ? opt.lookahead : ((nparts == 1 && !force_nccl) ? sx::kMaxLook : 1);
+  if (look > sx::kMaxLook) return fail(SIMPLEX_E_ARG, "lookahead larger than kMaxLook (16)");
+  if (look > 1 && (nparts > 1 || force_nccl))
+    return fail(SIMPLEX_E_ARG, "lookahead > 1 is implemented for one column part");
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -210,25 +220,46 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
     v.ld = roundup(v.w + 1, 16);
     v.nslot = (int)((v.ld / 2 + 31) / 32);
     sl.sel_grid = (int)std::min<long long>((v.rows + sx::kThreads - 1) / sx::kThreads, 2LL * sms);
-    // k_update: kUpdateCtasPerSm CTAs per SM; thread t owns column pair t mod (ld/2)
-    int occ = 1;
-    CK(sx::update_occupancy(&occ));
-    const long long half = v.ld / 2;
-    long long threads = (long long)std::min(occ, sx::kUpdateCtasPerSm) * sms * sx::kThreads;
-    threads = std::max(threads, roundup(half, sx::kThreads));
-    sl.q = (int)std::max(1LL, std::min<long long>(v.rows, threads / half));
-    sl.upd_grid = (int)((sl.q * half + sx::kThreads - 1) / sx::kThreads);
+    if (look > 1) {
+      // k_update_s: column chunks of cw doubles x row groups; all CTAs resident
+      sl.nc = (int)((v.ld + 2 * sx::kThreads - 1) / (2 * sx::kThreads));
+      sl.cw = (int)roundup((v.ld + sl.nc - 1) / sl.nc, 2);
+      int occ = 1;
+      CK(sx::update_s_occupancy(look, &occ, sx::update_s_smem(sl.cw, v.rows)));
+      if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
+      sl.Gr = (int)std::max(1LL, std::min<long long>(v.rows, (long long)occ * sms / sl.nc));
+    } else {
+      // k_update: kUpdateCtasPerSm CTAs per SM; thread t owns column pair t mod (ld/2)
+      int occ = 1;
+      CK(sx::update_occupancy(&occ));
+      const long long tpr = v.ld / 2;                      // threads per row
+      long long threads = (long long)std::min(occ, sx::kUpdateCtasPerSm) * sms * sx::kThreads;
+      threads = std::max(threads, roundup(tpr, sx::kThreads));
+      sl.q = (int)std::max(1LL, std::min<long long>(v.rows, threads / tpr));
+      sl.upd_grid = (int)((sl.q * tpr + sx::kThreads - 1) / sx::kThreads);
+    }
 
     RET(dalloc(&v.T, (size_t)v.rows * v.ld));
     RET(dalloc(&v.price, v.nslot));
     RET(dalloc(&v.col, v.rows + 2));
     RET(dalloc(&v.rownorm, v.ld));
-    RET(dalloc(&v.rcand, sl.sel_grid));
+    if (look > 1) {
+      sl.look_grid = sx::lookahead_cluster_size();
+      if (sl.look_grid < 1) return fail(SIMPLEX_E_CUDA, "look-ahead selection cluster cannot be scheduled");
+    }
+    RET(dalloc(&v.rcand, std::max(sl.sel_grid, sl.look_grid)));
     RET(dalloc(&v.basis, m));
     v.trace_cap = opt.record_trace ? cap : 0;
     RET(dalloc(&v.trace_k, std::max<long long>(v.trace_cap, 1)));
     RET(dalloc(&v.trace_r, std::max<long long>(v.trace_cap, 1)));
     RET(dalloc(&v.st, 1));
+    if (look > 1) {
+      RET(dalloc(&v.colS, (size_t)v.rows * sx::kMaxLook));
+      RET(dalloc(&v.prowS, (size_t)sx::kMaxLook * v.ld));
+      RET(dalloc(&v.R0, v.ld));
+      RET(dalloc(&v.RHS, v.rows));
+      RET(dalloc(&v.pcand, sl.look_grid));
+    }
   }
   RET(dalloc(&d_x, n));
   RET(dalloc(&d_y, m));
@@ -297,6 +328,15 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
 }
 
 simplex_err simplex_s::enqueue_pivot(int slot, int t) {
+  if (look > 1) {
+    // rank-s block: select up to `look` pivots ahead, then one pass applies them all
+    const Slab& sl = slabs[0];
+    CK(sx::launch_lookahead(sl.v, look, opt.tol_opt, opt.tol_piv, sl.look_grid, stream));
+    if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
+    CK(sx::launch_update_s(sl.v, look, sl.nc, sl.Gr, sl.cw, stream, pdl && !opt.time_kernels));
+    if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
+    return SIMPLEX_OK;
+  }
   // PDL (programmatic dependent launch) only between two of our kernels: not after an
   // NCCL collective or an event-record node.
   bool prev_is_ours = t > 0;   // previous node in the segment: k_update of the last pivot
@@ -330,13 +370,13 @@ simplex_err simplex_s::build_graphs() {
   if (graphs_ready) return SIMPLEX_OK;
   for (int slot = 0; slot < 2; ++slot) {
     if (opt.time_kernels) {
-      tev[slot].resize(2 * S);
+      tev[slot].resize(2 * steps_per_segment());
       for (auto& e : tev[slot]) CK(cudaEventCreate(&e));
     }
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     simplex_err e = SIMPLEX_OK;
-    for (int t = 0; t < S && e == SIMPLEX_OK; ++t) e = enqueue_pivot(slot, t);
+    for (int t = 0; t < steps_per_segment() && e == SIMPLEX_OK; ++t) e = enqueue_pivot(slot, t);
     if (e == SIMPLEX_OK) {
       cudaError_t ce = cudaMemcpyAsync(&h_state[slot], slabs[0].v.st, sizeof(sx::DevState),
                                        cudaMemcpyDeviceToHost, stream);
@@ -375,7 +415,7 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
       CK(cudaEventRecord(ev_done[slot], stream));
       ++launched;
       ++graph_launches;
-      kernel_launches += (long long)S * kernels_per_pivot();
+      kernel_launches += kernels_per_segment();
     }
     const int slot = (int)(completed & 1);
     CK(cudaEventSynchronize(ev_done[slot]));
@@ -383,7 +423,8 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
     ++completed;
     const long long piv = hs.it - seen;
     if (opt.time_kernels) {
-      for (long long q = 0; q < piv && q < S; ++q) {
+      const long long passes = look > 1 ? (piv + look - 1) / look : piv;   // k_update launches that did work
+      for (long long q = 0; q < passes && q < steps_per_segment(); ++q) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, tev[slot][2 * q], tev[slot][2 * q + 1]));
         upd_ms += ms;
@@ -449,6 +490,7 @@ void simplex_default_options(simplex_options* o) {
   o->virtual_ranks = 1;
   o->segment_pivots = 0;
   o->time_kernels = 0;
+  o->lookahead = 0;
 }
 
 simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* A, const double* b,

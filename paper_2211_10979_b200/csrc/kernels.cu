@@ -17,6 +17,7 @@
 // tableau equals the oracle's bit for bit after every pivot, for any tiling.
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "device.cuh"
@@ -46,7 +47,7 @@ __device__ __forceinline__ Cand warp_min(Cand c) {
 // Block-wide lexicographic argmin; every thread returns the result.  Contains
 // __syncthreads(): call from block-uniform control flow only.
 __device__ __forceinline__ Cand block_min(Cand c) {
-  __shared__ Cand sh[kThreads / 32];
+  __shared__ Cand sh[32];
   __shared__ Cand res;
   c = warp_min(c);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -74,6 +75,41 @@ __device__ __forceinline__ Cand ldcg_cand(const Cand* p) {
   c.v = __ldcg(&p->v);
   c.idx = __ldcg(&p->idx);
   return c;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 1-D TMA (cp.async.bulk) global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // ------------------------------------------------------------------ a0: build
@@ -135,6 +171,7 @@ __global__ void k_init_state(SlabView s, long long n, long long cap) {
     st->err = 0;
     st->ticket = 0;
     st->ticket2 = 0;
+    st->s_eff = 0;
   }
 }
 
@@ -367,6 +404,274 @@ __global__ void __launch_bounds__(kThreads) k_update(SlabView s, int q, double t
   }
 }
 
+// ------------------------------------------------------------------ rank-s look-ahead (NEXT #1)
+// Pivot t of a block needs only: the objective row of T^t (pricing), column k_t of T^t
+// (ratio test, staged col), the rhs column of T^t and row r_t of T^t (pivot row).  With the
+// block-start tableau T^0 untouched, each is T^0's entry followed by the chain of the
+// pending pivots 0..t-1 in the paper's order (PAPER.md:94 applied t times):
+//     x <- (i == r_u) ? prow_u[j] : fma(-col_u[i], prow_u[j], x),   u = 0 .. t-1
+// so selecting s pivots ahead costs O(s^2 (m + W)) and ONE pass then applies the s chains to
+// every element, in the same order: bitwise identical to s single pivots (reading c8).
+//
+// Barrier over the look-ahead kernel's CTAs: they form ONE thread-block cluster (up to 16
+// SMs), so this is the hardware cluster barrier (release/acquire at cluster scope).  Data
+// written by another CTA is read with ld.global.cg (L2), never through a stale L1.
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Fold per-CTA candidates (written before a grid barrier) in every CTA: same result everywhere.
+__device__ __forceinline__ Cand fold_cands(const Cand* c, int n) {
+  Cand b = cand_none();
+  for (int q = threadIdx.x; q < n; q += blockDim.x) b = cand_min(b, ldcg_cand(c + q));
+  return block_min(b);
+}
+
+// k_lookahead: one thread-block cluster (one CTA per SM) selecting up to S pivots.  Per pivot t:
+//   phase A (rows, grid-stride): RHS <- T^t's rhs (apply pivot t-1), column k of T^t by the
+//            chain from T^0, staged into colS[.][t], Step-2 candidates -> barrier -> r, p;
+//   phase B (columns, grid-stride): row r of T^t by the chain, prowS[t] = row / p, the
+//            objective row R0 <- T^{t+1}'s, Step-1 candidates -> barrier -> k of pivot t+1.
+// Every thread always owns the same rows / columns, so R0, RHS, colS[i][.] and prowS[.][j]
+// are only ever re-read by their writer; values written by OTHER CTAs are read with ld.cg.
+__global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, double tol_opt, double tol_piv) {
+  DevState* st = s.st;
+  __shared__ int sh_r[kMaxLook];
+  __shared__ double sh_pk[kMaxLook];       // prow_u[k] of the current entering column
+  __shared__ double sh_cr[kMaxLook];       // col_u[r] of the current pivot row
+  const int tid = threadIdx.x;
+  const unsigned int G = gridDim.x;
+  const long long gthreads = (long long)G * blockDim.x;
+  const long long gtid = blockIdx.x * (long long)blockDim.x + tid;
+  const int rows = s.rows;
+  const long long ld = s.ld;
+  const int w = s.w;
+  long long it = st->it;
+  int status = st->status;
+  const long long stop = st->stop_at;
+  const long long cap = st->cap;
+
+  // T^0's objective row and rhs column; Step 1 of the first pivot
+  Cand best = cand_none();
+  for (long long j = gtid; j < ld; j += gthreads) {
+    const double v = s.T[j];
+    s.R0[j] = v;
+    if (j < w && v < -tol_opt) best = cand_min(best, Cand{v, s.c0 + j});
+  }
+  for (long long i = gtid; i < rows; i += gthreads) s.RHS[i] = s.T[i * ld + w];
+  best = block_min(best);
+  if (tid == 0) s.pcand[blockIdx.x] = best;
+  cluster_barrier();
+  best = fold_cands(s.pcand, G);
+
+  int t = 0;
+  int r_prev = -1;
+  for (; t < S; ++t) {
+    if (status != kRunning || it >= stop) break;
+    if (best.idx == LLONG_MAX) { status = kOptimal; break; }                 // Step 1: optimal
+    const long long k = best.idx;
+    if (tid < t) sh_pk[tid] = __ldcg(s.prowS + (long long)tid * ld + k);
+    __syncthreads();
+    // ---- phase A: rows
+    const double pw_prev = t > 0 ? __ldcg(s.prowS + (long long)(t - 1) * ld + w) : 0.0;
+    Cand rb = cand_none();
+    for (long long i = gtid; i < rows; i += gthreads) {
+      double h = s.RHS[i];
+      if (t > 0) h = (i == r_prev) ? pw_prev : __fma_rn(-s.colS[i * kMaxLook + t - 1], pw_prev, h);
+      s.RHS[i] = h;
+      double x = s.T[i * ld + k];
+      double cu[kMaxLook];                   // issue the row's pending-column loads together
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u) cu[u] = u < t ? s.colS[i * kMaxLook + u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u)
+        if (u < t) x = (i == sh_r[u]) ? sh_pk[u] : __fma_rn(-cu[u], sh_pk[u], x);
+      s.colS[i * kMaxLook + t] = x;
+      if (i >= 1 && x > tol_piv) rb = cand_min(rb, Cand{__ddiv_rn(h, x), i});   // Step 2
+    }
+    rb = block_min(rb);
+    if (tid == 0) s.rcand[blockIdx.x] = rb;
+    cluster_barrier();
+    rb = fold_cands(s.rcand, G);
+    if (rb.idx == LLONG_MAX) {                                                 // unbounded
+      status = kUnbounded;
+      if (gtid == 0) st->k = (int)k;
+      break;
+    }
+    if (it >= cap) { status = kIterLimit; break; }                            // reading c12
+    const int r = (int)rb.idx;
+    const double p = __ldcg(s.colS + (long long)r * kMaxLook + t);
+    if (tid < t) sh_cr[tid] = __ldcg(s.colS + (long long)r * kMaxLook + tid);
+    __syncthreads();
+    // ---- phase B: columns (pivot row of T^t, normalized; objective row of T^{t+1})
+    const double a0 = -__ldcg(s.colS + t);                                    // col_t[0]
+    const double* Tr = s.T + (long long)r * ld;
+    double* prow = s.prowS + (long long)t * ld;
+    best = cand_none();
+    for (long long j = gtid; j < ld; j += gthreads) {
+      double x = Tr[j];
+      double pu[kMaxLook];                   // issue the column's pending-row loads together
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? s.prowS[(long long)u * ld + j] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u)
+        if (u < t) x = (r == sh_r[u]) ? pu[u] : __fma_rn(-sh_cr[u], pu[u], x);
+      const double pj = __ddiv_rn(x, p);
+      prow[j] = pj;
+      const double v = __fma_rn(a0, pj, s.R0[j]);
+      s.R0[j] = v;
+      if (j < w && v < -tol_opt) best = cand_min(best, Cand{v, s.c0 + j});   // Step 1 of t+1
+    }
+    if (tid == 0) sh_r[t] = r;
+    if (gtid == 0) {
+      st->rs[t] = r;
+      s.basis[r - 1] = (int)k;
+      if (it < s.trace_cap) {
+        s.trace_k[it] = (int)k;
+        s.trace_r[it] = r;
+      }
+    }
+    ++it;
+    r_prev = r;
+    best = block_min(best);
+    if (tid == 0) s.pcand[blockIdx.x] = best;
+    cluster_barrier();
+    best = fold_cands(s.pcand, G);
+  }
+  if (gtid == 0) {
+    st->status = status;
+    st->it = it;
+    st->s_eff = t;
+    st->go = t > 0;
+    st->pend_r = -1;
+  }
+}
+
+// k_update_s: the rank-s pass, TMA-pipelined.  CTA b owns column chunk c = b mod nc
+// (cw doubles, one double2 per consumer thread) and rows g, g+Gr, g+2Gr, ... (g = b div nc),
+// so all CTAs sweep Gr consecutive rows at a time: the chip-wide HBM front stays contiguous.
+// A producer warp streams each row segment T[i][chunk] and the row's pivot-column entries
+// colS[i][0..15] into a K-stage shared-memory ring with 1-D TMA (cp.async.bulk + mbarrier
+// complete_tx), so the bytes in flight cost shared memory, not registers.  The 8 consumer
+// warps hold prow_u[j] (u < s) in registers, read a row's values from shared memory and
+// apply the chain  x <- fma(-col_u[i], prow_u[j], x), u = 0 .. s-1  (the oracle's order and
+// rounding), then store with 128-bit st.global.  The <= s pivot rows are not stored by the
+// stream (bitmap) but written at the end from their last normalized value prow_u, chained
+// over the later pivots of the block.
+template <int S, int R, int K>
+__global__ void __launch_bounds__(kThreads + 32) k_update_s(SlabView s, int nc, int Gr, int cw) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const DevState* st = s.st;
+  if (!st->go) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sT = reinterpret_cast<double*>(smem_raw);                 // [K][R][cw]
+  double* sC = sT + (size_t)K * R * cw;                              // [K][R][kMaxLook]
+  unsigned int* mark = reinterpret_cast<unsigned int*>(sC + (size_t)K * R * kMaxLook);
+  __shared__ __align__(8) uint64_t full[K];
+  __shared__ __align__(8) uint64_t empty[K];
+  __shared__ int sh_r[S];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int se = st->s_eff;
+  const int rows = s.rows;
+  const long long ld = s.ld;
+  const int nwords = (rows + 31) >> 5;
+  for (int i = tid; i < nwords; i += blockDim.x) mark[i] = 0u;
+  if (tid < S) sh_r[tid] = tid < se ? st->rs[tid] : -1;
+  if (tid == 0) {
+    for (int k = 0; k < K; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], kThreads / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid < se) atomicOr(&mark[sh_r[tid] >> 5], 1u << (sh_r[tid] & 31));
+  __syncthreads();
+
+  const int c = blockIdx.x % nc;
+  const int g = blockIdx.x / nc;
+  const long long j0 = (long long)c * cw;
+  const int jn = (int)min((long long)cw, ld - j0);                    // doubles in this chunk
+  const int nr = rows > g ? (rows - g + Gr - 1) / Gr : 0;             // rows of this CTA
+  const int nst = (nr + R - 1) / R;
+
+  if (warp == kThreads / 32) {                                        // ---- producer warp
+    if (lane == 0) {
+      for (int n = 0; n < nst; ++n) {
+        const int k = n % K;
+        if (n >= K) mbar_wait(&empty[k], ((n / K) - 1) & 1);
+        const int rin = min(R, nr - n * R);
+        mbar_arrive_expect_tx(&full[k], (uint32_t)(rin * (jn + kMaxLook) * sizeof(double)));
+        for (int rr = 0; rr < rin; ++rr) {
+          const long long i = g + (long long)(n * R + rr) * Gr;
+          bulk_g2s(sT + ((size_t)k * R + rr) * cw, s.T + i * ld + j0, (uint32_t)(jn * sizeof(double)), &full[k]);
+          bulk_g2s(sC + ((size_t)k * R + rr) * kMaxLook, s.colS + i * kMaxLook,
+                   (uint32_t)(kMaxLook * sizeof(double)), &full[k]);
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumer warps
+  const int jl = 2 * tid;
+  const bool act = jl < jn;
+  const long long j = j0 + jl;
+  double2 pr[S];
+#pragma unroll
+  for (int u = 0; u < S; ++u)
+    pr[u] = (act && u < se) ? *reinterpret_cast<const double2*>(s.prowS + (long long)u * ld + j)
+                            : make_double2(0.0, 0.0);
+  for (int n = 0; n < nst; ++n) {
+    const int k = n % K;
+    mbar_wait(&full[k], (n / K) & 1);
+    const int rin = min(R, nr - n * R);
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr < rin && act) {
+        const int i = g + (n * R + rr) * Gr;
+        double2 v = *reinterpret_cast<const double2*>(sT + ((size_t)k * R + rr) * cw + jl);
+        const double* cc = sC + ((size_t)k * R + rr) * kMaxLook;
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          if (u < se) {
+            const double a = -cc[u];
+            v.x = __fma_rn(a, pr[u].x, v.x);
+            v.y = __fma_rn(a, pr[u].y, v.y);
+          }
+        }
+        if (!((mark[i >> 5] >> (i & 31)) & 1u)) *reinterpret_cast<double2*>(s.T + (long long)i * ld + j) = v;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[k]);
+  }
+  if (!act) return;
+  // pivot rows of this chunk owned by this row group: from the LAST time each was the
+  // pivot row, chained over the later pivots of the block
+#pragma unroll
+  for (int u = 0; u < S; ++u) {
+    if (u >= se) break;
+    const int r = sh_r[u];
+    if (r % Gr != g) continue;
+    bool last = true;
+    for (int u2 = u + 1; u2 < se; ++u2) last &= (sh_r[u2] != r);
+    if (!last) continue;
+    double2 v = pr[u];
+    const double* cr = s.colS + (long long)r * kMaxLook;
+#pragma unroll
+    for (int u2 = 0; u2 < S; ++u2) {
+      if (u2 > u && u2 < se) {
+        const double a = -cr[u2];
+        v.x = __fma_rn(a, pr[u2].x, v.x);
+        v.y = __fma_rn(a, pr[u2].y, v.y);
+      }
+    }
+    *reinterpret_cast<double2*>(s.T + (long long)r * ld + j) = v;
+  }
+}
+
 // ------------------------------------------------------------------ flush / extract / hash
 __global__ void __launch_bounds__(1024) k_flush(SlabView s) {
   const int pend = s.st->pend_r;
@@ -456,11 +761,12 @@ cudaError_t launch_price0(const SlabView& s, double tol_opt, cudaStream_t st) {
 }
 
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_ex(void (*kern)(KArgs...), int grid, int block, cudaStream_t st, bool pdl, Args... args) {
+static cudaError_t launch_ex(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, bool pdl,
+                             Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -471,11 +777,11 @@ static cudaError_t launch_ex(void (*kern)(KArgs...), int grid, int block, cudaSt
 }
 
 cudaError_t launch_pack(const SlabView& s, double* send, int grid, cudaStream_t st, bool pdl) {
-  return launch_ex(k_pack, grid, kThreads, st, pdl, s, send);
+  return launch_ex(k_pack, grid, kThreads, 0, st, pdl, s, send);
 }
 
 cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int grid, cudaStream_t st, bool pdl) {
-  return launch_ex(k_select, grid, kThreads, st, pdl, s, x, tol_piv);
+  return launch_ex(k_select, grid, kThreads, 0, st, pdl, s, x, tol_piv);
 }
 
 cudaError_t update_occupancy(int* blocks_per_sm) {
@@ -483,7 +789,106 @@ cudaError_t update_occupancy(int* blocks_per_sm) {
 }
 
 cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st, bool pdl) {
-  return launch_ex(k_update<kUpdateRows>, grid, kThreads, st, pdl, s, q, tol_opt);
+  return launch_ex(k_update<kUpdateRows>, grid, kThreads, 0, st, pdl, s, q, tol_opt);
+}
+
+static cudaLaunchConfig_t lookahead_config(int cluster, cudaStream_t st, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(kLookThreads);
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+// Largest cluster (16, else 8, 4, 2, 1 CTAs) the device can co-schedule for k_lookahead.
+int lookahead_cluster_size() {
+  cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int c : {16, 8, 4, 2, 1}) {
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = lookahead_config(c, nullptr, attr);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_lookahead, &cfg) == cudaSuccess && n >= 1) return c;
+    cudaGetLastError();
+  }
+  return 0;
+}
+
+cudaError_t launch_lookahead(const SlabView& s, int S, double tol_opt, double tol_piv, int cluster, cudaStream_t st) {
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, st, attr);
+  return cudaLaunchKernelEx(&cfg, k_lookahead, s, S, tol_opt, tol_piv);
+}
+
+// k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
+// SIMPLEX_PASS_CFG selects one for experiments (default 0).
+struct PassCfg { int R, K; };
+static const PassCfg kPassCfgs[] = {{2, 6}, {4, 4}, {1, 8}, {2, 8}};
+static int pass_cfg() {
+  static int c = [] {
+    const char* e = std::getenv("SIMPLEX_PASS_CFG");
+    const int v = e ? std::atoi(e) : 0;
+    return (v >= 0 && v < 4) ? v : 0;
+  }();
+  return c;
+}
+int update_s_max(int S) { return S <= 4 ? 4 : S <= 8 ? 8 : 16; }
+
+size_t update_s_smem(int cw, int rows) {
+  const PassCfg c = kPassCfgs[pass_cfg()];
+  return (size_t)c.K * c.R * (cw + kMaxLook) * sizeof(double) + (size_t)((rows + 31) / 32) * sizeof(unsigned int);
+}
+
+template <int S, int R, int K>
+static cudaError_t pass_prepare(size_t smem, int* occ) {
+  auto kern = k_update_s<S, R, K>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, kThreads + 32, smem);
+}
+
+template <int R, int K>
+static cudaError_t pass_prepare_s(int S, size_t smem, int* occ) {
+  switch (update_s_max(S)) {
+    case 4: return pass_prepare<4, R, K>(smem, occ);
+    case 8: return pass_prepare<8, R, K>(smem, occ);
+    default: return pass_prepare<16, R, K>(smem, occ);
+  }
+}
+
+cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem) {
+  switch (pass_cfg()) {
+    case 1: return pass_prepare_s<4, 4>(S, smem, blocks_per_sm);
+    case 2: return pass_prepare_s<1, 8>(S, smem, blocks_per_sm);
+    case 3: return pass_prepare_s<2, 8>(S, smem, blocks_per_sm);
+    default: return pass_prepare_s<2, 6>(S, smem, blocks_per_sm);
+  }
+}
+
+template <int R, int K>
+static cudaError_t pass_launch(const SlabView& s, int S, int nc, int Gr, int cw, size_t smem, cudaStream_t st,
+                               bool pdl) {
+  const int grid = nc * Gr;
+  switch (update_s_max(S)) {
+    case 4: return launch_ex(k_update_s<4, R, K>, grid, kThreads + 32, smem, st, pdl, s, nc, Gr, cw);
+    case 8: return launch_ex(k_update_s<8, R, K>, grid, kThreads + 32, smem, st, pdl, s, nc, Gr, cw);
+    default: return launch_ex(k_update_s<16, R, K>, grid, kThreads + 32, smem, st, pdl, s, nc, Gr, cw);
+  }
+}
+
+cudaError_t launch_update_s(const SlabView& s, int S, int nc, int Gr, int cw, cudaStream_t st, bool pdl) {
+  const size_t smem = update_s_smem(cw, s.rows);
+  switch (pass_cfg()) {
+    case 1: return pass_launch<4, 4>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 2: return pass_launch<1, 8>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 3: return pass_launch<2, 8>(s, S, nc, Gr, cw, smem, st, pdl);
+    default: return pass_launch<2, 6>(s, S, nc, Gr, cw, smem, st, pdl);
+  }
 }
 
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st) {

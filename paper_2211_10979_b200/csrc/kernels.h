@@ -18,6 +18,12 @@ cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int
                           bool pdl);
 cudaError_t update_occupancy(int* blocks_per_sm);
 cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st, bool pdl);
+cudaError_t launch_lookahead(const SlabView& s, int S, double tol_opt, double tol_piv, int cluster, cudaStream_t st);
+int lookahead_cluster_size();
+int update_s_max(int S);
+size_t update_s_smem(int cw, int rows);
+cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem);
+cudaError_t launch_update_s(const SlabView& s, int S, int nc, int Gr, int cw, cudaStream_t st, bool pdl);
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st);
 cudaError_t launch_extract(const SlabView& s, long long n, double* x, double* y, double* obj, cudaStream_t st);
 cudaError_t launch_hash(const SlabView& s, long long Wg, int include_rhs, unsigned long long* out,

@@ -1,0 +1,42 @@
+"""Per-source-line stall samples / instructions from an ncu report (needs -lineinfo).
+
+    python scripts/ncu_hotspots.py report.ncu-rep [top]
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+rep = sys.argv[1]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+lines = out.splitlines()
+hdr_i = next(i for i, l in enumerate(lines) if l.startswith('"Line No"'))
+rows = list(csv.reader(io.StringIO("\n".join(lines[hdr_i:]))))
+hdr = rows[0]
+i_line, i_src = 0, 1
+i_stall = hdr.index("Warp Stall Sampling (All Samples)")
+i_inst = hdr.index("Instructions Executed")
+agg = defaultdict(lambda: [0.0, 0.0, ""])
+cur = None
+for r in rows[1:]:
+    if len(r) <= i_inst:
+        continue
+    if r[i_line].strip() and not r[i_line].strip().isdigit():
+        continue
+    if r[i_line].strip():
+        cur = (int(r[i_line]), r[i_src].strip()[:100])
+    if cur is None:
+        continue
+    try:
+        agg[cur[0]][0] += float(r[i_stall] or 0)
+        agg[cur[0]][1] += float(r[i_inst] or 0)
+        agg[cur[0]][2] = cur[1]
+    except ValueError:
+        pass
+ts = sum(v[0] for v in agg.values()) or 1
+ti = sum(v[1] for v in agg.values()) or 1
+for ln, (st, ins, src) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+    print(f"{100 * st / ts:5.1f}% stall {100 * ins / ti:5.1f}% inst  L{ln}: {src}")

@@ -1,0 +1,134 @@
+"""GPU parity of the rank-s look-ahead path: s pivots selected
+ahead from chained corrections, one tableau pass applies them.  The claim is BITWISE
+identity with s single pivots, so every check is exact equality with the oracle."""
+import os
+
+import numpy as np
+import pytest
+
+import lpgen
+import oracle
+from lpgen import fixtures as F
+
+from test_gpu_parity import GOLD, GOLDEN_DIR, assert_same, gpu_solve  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+LOOKS = [2, 4, 8, 16]
+
+
+@pytest.fixture(scope="module")
+def sx(cuda_device):
+    import paper_2211_10979_b200 as sx
+    return sx
+
+
+@pytest.mark.parametrize("look", LOOKS)
+@pytest.mark.parametrize("name", ["classic", "chvatal", "unbounded", "beale", "entering_tie", "ratio_tie",
+                                  "zero_iteration"])
+def test_worked_examples(sx, name, look):
+    if name == "classic":
+        A, b, c = F.classic()
+    elif name == "chvatal":
+        A, b, c = F.chvatal()
+    elif name == "unbounded":
+        A, b, c = F.unbounded_1d()
+    elif name == "beale":
+        A, b, c = F.beale()
+    else:
+        g = GOLD[name]
+        A, b, c = (np.array(g[k], float) for k in ("A", "b", "c"))
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=look), o)
+
+
+@pytest.mark.parametrize("look", LOOKS)
+def test_klee_minty(sx, look):
+    A, b, c = F.klee_minty(9)                      # 511 pivots, many repeated pivot rows
+    o = oracle.solve(A, b, c, max_pivots=600, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, max_pivots=600, lookahead=look), o)
+
+
+@pytest.mark.parametrize("look", LOOKS)
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_dense_64(sx, seed, look):
+    A, b, c = lpgen.dense_lp(64, 64, seed)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=look), o)
+
+
+@pytest.mark.parametrize("look", [3, 8, 16])
+@pytest.mark.parametrize("seed", range(10))
+def test_tie_heavy(sx, seed, look):
+    rng = np.random.default_rng(seed)
+    m, n = int(rng.integers(3, 40)), int(rng.integers(3, 40))
+    A, b, c = F.tie_heavy(m, n, seed)
+    A[:, A.sum(axis=0) == 0] = 1.0
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=look), o)
+
+
+@pytest.mark.parametrize("look", [5, 16])
+@pytest.mark.parametrize("m,n", [(1, 1), (1, 700), (700, 1), (3, 1500), (257, 513), (1100, 90)])
+def test_ragged_shapes(sx, m, n, look):
+    A, b, c = lpgen.dense_lp(m, n, 1000 + m + n)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=look), o)
+
+
+def test_iteration_cap_inside_a_block(sx):
+    A, b, c = F.klee_minty(6)                      # 63 pivots; cap 21 falls inside a block of 8
+    o = oracle.solve(A, b, c, max_pivots=21, keep_tableau=True)
+    assert o.status == oracle.ITERATION_LIMIT
+    assert_same(gpu_solve(sx, A, b, c, max_pivots=21, lookahead=8), o)
+
+
+def test_iterate_stepwise_bitwise(sx):
+    A, b, c = lpgen.dense_lp(64, 64, 3)
+    with sx.Simplex(A, b, c, lookahead=8, segment_pivots=16) as s:
+        done_total = 0
+        for step in (1, 3, 7, 8, 2, 16):
+            done, st = s.iterate(step)
+            done_total += done
+            o = oracle.solve(A, b, c, stop_after=done_total, keep_tableau=True)
+            T, _ = s.tableau()
+            assert np.array_equal(T, o.T), done_total
+            if st != sx.RUNNING:
+                break
+
+
+@pytest.mark.parametrize("key", [(1000, 1000, 1), (4000, 4000, 1)])
+@pytest.mark.parametrize("look", [8, 16])
+def test_golden(sx, key, look):
+    g = np.load(os.path.join(GOLDEN_DIR, "dense_%dx%d_s%d.npz" % key))
+    A, b, c = lpgen.dense_lp(*key)
+    with sx.Simplex(A, b, c, lookahead=look) as s:
+        st = s.solve()
+        x, y, obj, piv, _ = s.solution()
+        k, r = s.trace()
+        h = s.tableau_hash()
+    assert st == int(g["status"]) and piv == int(g["pivots"])
+    assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+    assert obj == float(g["objective"]) and np.array_equal(y, g["y"])
+    assert h == int(g["tableau_hash"])
+
+
+def test_golden_8000_default_path(sx):
+    """The bench workload through the library default (rank-16 look-ahead) against the
+    oracle's full 8000x8000 solve (tests/golden, ~69 min of single-thread oracle)."""
+    g = np.load(os.path.join(GOLDEN_DIR, "dense_8000x8000_s1.npz"))
+    A, b, c = lpgen.dense_lp(8000, 8000, 1)
+    with sx.Simplex(A, b, c) as s:
+        st = s.solve()
+        x, y, obj, piv, _ = s.solution()
+        k, r = s.trace()
+        h = s.tableau_hash()
+    assert st == int(g["status"]) and piv == int(g["pivots"]) == 25395
+    assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+    assert obj == float(g["objective"]) and np.array_equal(y, g["y"])
+    xs = np.zeros(8000)
+    xs[g["x_idx"]] = g["x_val"]
+    assert np.array_equal(x, xs)
+    assert h == int(g["tableau_hash"])
+    cert = oracle.certificate(A, b, c, x, y)
+    assert not cert.violations, cert.violations

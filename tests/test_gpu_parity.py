@@ -29,6 +29,7 @@ def sx(cuda_device):
 
 
 def gpu_solve(sx, A, b, c, **kw):
+    kw.setdefault("lookahead", 1)           # this file covers the one-pivot-per-pass path
     with sx.Simplex(A, b, c, **kw) as s:
         st = s.solve()
         x, y, obj, piv, st2 = s.solution()
@@ -123,7 +124,7 @@ def test_virtual_ranks_ties(sx):
 def test_iterate_stepwise_bitwise(sx):
     # after EVERY pivot the device tableau equals the oracle's bit for bit
     A, b, c = lpgen.dense_lp(64, 64, 3)
-    with sx.Simplex(A, b, c, segment_pivots=4) as s:
+    with sx.Simplex(A, b, c, segment_pivots=4, lookahead=1) as s:
         for t in range(1, 40):
             done, st = s.iterate(1)
             o = oracle.solve(A, b, c, stop_after=t, keep_tableau=True)
@@ -139,7 +140,7 @@ def test_iterate_stepwise_bitwise(sx):
 def test_iterate_then_solve_equals_solve(sx):
     A, b, c = lpgen.dense_lp(300, 400, 9)
     o = oracle.solve(A, b, c, keep_tableau=True)
-    with sx.Simplex(A, b, c) as s:
+    with sx.Simplex(A, b, c, lookahead=1) as s:
         d1, st = s.iterate(17)
         assert d1 == 17 and st == sx.RUNNING
         d2, st = s.iterate(5)
@@ -158,7 +159,7 @@ def test_reset_and_device_io(sx):
     A2, b2, c2 = lpgen.dense_lp(200, 150, 5)
     o2 = oracle.solve(A2, b2, c2)
     dA, db, dc = (torch.from_numpy(v).cuda() for v in (A, b, c))
-    with sx.Simplex(dA, db, dc) as s:
+    with sx.Simplex(dA, db, dc, lookahead=1) as s:
         assert s.solve() == sx.OPTIMAL
         dx = torch.empty(150, dtype=torch.float64, device="cuda")
         dy = torch.empty(200, dtype=torch.float64, device="cuda")
@@ -200,7 +201,7 @@ def test_golden_full_size(sx, key):
         pytest.fail("missing golden file " + path)
     g = np.load(path)
     A, b, c = lpgen.dense_lp(*key)
-    with sx.Simplex(A, b, c) as s:
+    with sx.Simplex(A, b, c, lookahead=1) as s:
         st = s.solve()
         x, y, obj, piv, _ = s.solution()
         k, r = s.trace()
@@ -234,16 +235,18 @@ def test_wide_prefix_20000x40000(sx):
     path = os.path.join(GOLDEN_DIR, "dense_20000x40000_s1_p32.npz")
     g = np.load(path)
     A, b, c = lpgen.dense_lp(20000, 40000, 1)
-    with sx.Simplex(A, b, c) as s:
-        done, st = s.iterate(32)
-        assert done == 32 and st == sx.RUNNING
-        k, r = s.trace()
-        h = s.tableau_hash()
-        x, y, obj, piv, _ = s.solution()
-    assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
-    assert obj == float(g["objective"])
-    assert np.array_equal(y, g["y"])
-    xs = np.zeros(40000)
-    xs[g["x_idx"]] = g["x_val"]
-    assert np.array_equal(x, xs)
-    assert h == int(g["tableau_hash"])
+    for look in (1, 16):                     # one pivot per pass, and two rank-16 blocks
+        with sx.Simplex(A, b, c, lookahead=look) as s:
+            done, st = s.iterate(32)
+            assert done == 32 and st == sx.RUNNING
+            k, r = s.trace()
+            h = s.tableau_hash()
+            x, y, obj, piv, _ = s.solution()
+        assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+        assert obj == float(g["objective"])
+        assert np.array_equal(y, g["y"])
+        xs = np.zeros(40000)
+        xs[g["x_idx"]] = g["x_val"]
+        assert np.array_equal(x, xs)
+        assert h == int(g["tableau_hash"])
+
