@@ -420,49 +420,84 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// Fold per-CTA candidates (written before a grid barrier) in every CTA: same result everywhere.
-__device__ __forceinline__ Cand fold_cands(const Cand* c, int n) {
-  Cand b = cand_none();
-  for (int q = threadIdx.x; q < n; q += blockDim.x) b = cand_min(b, ldcg_cand(c + q));
-  return block_min(b);
+// Cluster-wide lexicographic argmin, identical in every CTA of the cluster.  Each CTA
+// reduces its warps, then warp 0 writes the CTA's candidate straight into slot[rank] of
+// EVERY CTA's shared memory (DSMEM st.shared::cluster), one cluster barrier, and every
+// CTA folds its local copy.  `slot` is double-buffered by `ph` (a CTA can be at most one
+// reduction ahead of another), so two consecutive reductions never share a slot.
+__device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph) {
+  __shared__ Cand sh_w[32];
+  __shared__ Cand sh_res;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned int rank, nct;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(nct));
+  c = warp_min(c);
+  if (lane == 0) sh_w[wid] = c;
+  __syncthreads();
+  if (wid == 0) {
+    Cand t = lane < (int)(blockDim.x >> 5) ? sh_w[lane] : cand_none();
+    t = warp_min(t);
+    if (lane < (int)nct) {
+      const uint32_t local = smem_u32(slot + ph * 16 + rank);
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(lane));
+      asm volatile("st.shared::cluster.v2.b64 [%0], {%1, %2};" ::"r"(remote), "l"(__double_as_longlong(t.v)),
+                   "l"(t.idx)
+                   : "memory");
+    }
+  }
+  cluster_barrier();
+  if (wid == 0) {
+    Cand t = lane < (int)nct ? slot[ph * 16 + lane] : cand_none();
+    t = warp_min(t);
+    if (lane == 0) sh_res = t;
+  }
+  __syncthreads();
+  return sh_res;
 }
 
 // k_lookahead: one thread-block cluster (one CTA per SM) selecting up to S pivots.  Per pivot t:
 //   phase A (rows, grid-stride): RHS <- T^t's rhs (apply pivot t-1), column k of T^t by the
-//            chain from T^0, staged into colS[.][t], Step-2 candidates -> barrier -> r, p;
+//            chain from T^0, staged into colS[.][t], Step-2 candidates -> cluster argmin -> r;
 //   phase B (columns, grid-stride): row r of T^t by the chain, prowS[t] = row / p, the
-//            objective row R0 <- T^{t+1}'s, Step-1 candidates -> barrier -> k of pivot t+1.
+//            objective row R0 <- T^{t+1}'s, Step-1 candidates -> cluster argmin -> k of t+1.
 // Every thread always owns the same rows / columns, so R0, RHS, colS[i][.] and prowS[.][j]
-// are only ever re-read by their writer; values written by OTHER CTAs are read with ld.cg.
+// are only re-read by their writer; values written by OTHER CTAs are read with ld.cg.  All
+// loads a phase needs (per-step scalars, the T entry, the pending chain operands) are issued
+// before the first dependent use, so each phase costs about one memory latency.
 __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, double tol_opt, double tol_piv) {
   DevState* st = s.st;
   __shared__ int sh_r[kMaxLook];
-  __shared__ double sh_pk[kMaxLook];       // prow_u[k] of the current entering column
-  __shared__ double sh_cr[kMaxLook];       // col_u[r] of the current pivot row
-  const int tid = threadIdx.x;
-  const unsigned int G = gridDim.x;
-  const long long gthreads = (long long)G * blockDim.x;
-  const long long gtid = blockIdx.x * (long long)blockDim.x + tid;
+  __shared__ __align__(16) Cand slot[2 * 16];
+  extern __shared__ unsigned int piv_mark[];          // rows already pivot rows in this block
+  const long long gthreads = (long long)gridDim.x * blockDim.x;
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int rows = s.rows;
   const long long ld = s.ld;
   const int w = s.w;
+  const double* __restrict__ T = s.T;
+  double* __restrict__ colS = s.colS;
+  double* __restrict__ prowS = s.prowS;
+  double* __restrict__ R0 = s.R0;
+  double* __restrict__ RHS = s.RHS;
   long long it = st->it;
   int status = st->status;
   const long long stop = st->stop_at;
   const long long cap = st->cap;
+  int ph = 0;
+  for (int q = threadIdx.x; q < (rows + 31) / 32; q += blockDim.x) piv_mark[q] = 0u;
 
   // T^0's objective row and rhs column; Step 1 of the first pivot
   Cand best = cand_none();
   for (long long j = gtid; j < ld; j += gthreads) {
-    const double v = s.T[j];
-    s.R0[j] = v;
+    const double v = T[j];
+    R0[j] = v;
     if (j < w && v < -tol_opt) best = cand_min(best, Cand{v, s.c0 + j});
   }
-  for (long long i = gtid; i < rows; i += gthreads) s.RHS[i] = s.T[i * ld + w];
-  best = block_min(best);
-  if (tid == 0) s.pcand[blockIdx.x] = best;
-  cluster_barrier();
-  best = fold_cands(s.pcand, G);
+  for (long long i = gtid; i < rows; i += gthreads) RHS[i] = T[i * ld + w];
+  best = cluster_min(best, slot, ph);
+  ph ^= 1;
 
   int t = 0;
   int r_prev = -1;
@@ -470,29 +505,34 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
     if (status != kRunning || it >= stop) break;
     if (best.idx == LLONG_MAX) { status = kOptimal; break; }                 // Step 1: optimal
     const long long k = best.idx;
-    if (tid < t) sh_pk[tid] = __ldcg(s.prowS + (long long)tid * ld + k);
-    __syncthreads();
     // ---- phase A: rows
-    const double pw_prev = t > 0 ? __ldcg(s.prowS + (long long)(t - 1) * ld + w) : 0.0;
+    double pk[kMaxLook];                                // prow_u[k], u < t (L2, same for all rows)
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) pk[u] = u < t ? __ldcg(prowS + (long long)u * ld + k) : 0.0;
+    const double pw_prev = t > 0 ? __ldcg(prowS + (long long)(t - 1) * ld + w) : 0.0;
     Cand rb = cand_none();
     for (long long i = gtid; i < rows; i += gthreads) {
-      double h = s.RHS[i];
-      if (t > 0) h = (i == r_prev) ? pw_prev : __fma_rn(-s.colS[i * kMaxLook + t - 1], pw_prev, h);
-      s.RHS[i] = h;
-      double x = s.T[i * ld + k];
-      double cu[kMaxLook];                   // issue the row's pending-column loads together
+      double x = T[i * ld + k];
+      double h = RHS[i];
+      double cu[kMaxLook];                              // this row's pending-column entries
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) cu[u] = u < t ? s.colS[i * kMaxLook + u] : 0.0;
+      for (int u = 0; u < kMaxLook; ++u) cu[u] = u < t ? colS[i * kMaxLook + u] : 0.0;
+      if (t > 0) h = (i == r_prev) ? pw_prev : __fma_rn(-colS[i * kMaxLook + t - 1], pw_prev, h);
+      RHS[i] = h;
+      if ((piv_mark[i >> 5] >> (i & 31)) & 1u) {       // row i was a pivot row of this block
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u)
-        if (u < t) x = (i == sh_r[u]) ? sh_pk[u] : __fma_rn(-cu[u], sh_pk[u], x);
-      s.colS[i * kMaxLook + t] = x;
+        for (int u = 0; u < kMaxLook; ++u)
+          if (u < t) x = (i == sh_r[u]) ? pk[u] : __fma_rn(-cu[u], pk[u], x);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kMaxLook; ++u)
+          if (u < t) x = __fma_rn(-cu[u], pk[u], x);
+      }
+      colS[i * kMaxLook + t] = x;
       if (i >= 1 && x > tol_piv) rb = cand_min(rb, Cand{__ddiv_rn(h, x), i});   // Step 2
     }
-    rb = block_min(rb);
-    if (tid == 0) s.rcand[blockIdx.x] = rb;
-    cluster_barrier();
-    rb = fold_cands(s.rcand, G);
+    rb = cluster_min(rb, slot, ph);
+    ph ^= 1;
     if (rb.idx == LLONG_MAX) {                                                 // unbounded
       status = kUnbounded;
       if (gtid == 0) st->k = (int)k;
@@ -500,29 +540,38 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
     }
     if (it >= cap) { status = kIterLimit; break; }                            // reading c12
     const int r = (int)rb.idx;
-    const double p = __ldcg(s.colS + (long long)r * kMaxLook + t);
-    if (tid < t) sh_cr[tid] = __ldcg(s.colS + (long long)r * kMaxLook + tid);
-    __syncthreads();
     // ---- phase B: columns (pivot row of T^t, normalized; objective row of T^{t+1})
-    const double a0 = -__ldcg(s.colS + t);                                    // col_t[0]
-    const double* Tr = s.T + (long long)r * ld;
-    double* prow = s.prowS + (long long)t * ld;
+    double cr[kMaxLook];                                // col_u[r], u < t (L2, same for all columns)
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? __ldcg(colS + (long long)r * kMaxLook + u) : 0.0;
+    const double p = __ldcg(colS + (long long)r * kMaxLook + t);
+    const double a0 = -__ldcg(colS + t);                                      // col_t[0]
+    const double* Tr = T + (long long)r * ld;
+    double* prow = prowS + (long long)t * ld;
+    unsigned int rmask = 0u;                            // bit u: r was already pivot row u
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u)
+      if (u < t && sh_r[u] == r) rmask |= 1u << u;
     best = cand_none();
     for (long long j = gtid; j < ld; j += gthreads) {
       double x = Tr[j];
-      double pu[kMaxLook];                   // issue the column's pending-row loads together
+      const double r0 = R0[j];
+      double pu[kMaxLook];                              // this column's pending-row entries
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? s.prowS[(long long)u * ld + j] : 0.0;
+      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? prowS[(long long)u * ld + j] : 0.0;
 #pragma unroll
       for (int u = 0; u < kMaxLook; ++u)
-        if (u < t) x = (r == sh_r[u]) ? pu[u] : __fma_rn(-sh_cr[u], pu[u], x);
+        if (u < t) x = ((rmask >> u) & 1u) ? pu[u] : __fma_rn(-cr[u], pu[u], x);
       const double pj = __ddiv_rn(x, p);
       prow[j] = pj;
-      const double v = __fma_rn(a0, pj, s.R0[j]);
-      s.R0[j] = v;
+      const double v = __fma_rn(a0, pj, r0);
+      R0[j] = v;
       if (j < w && v < -tol_opt) best = cand_min(best, Cand{v, s.c0 + j});   // Step 1 of t+1
     }
-    if (tid == 0) sh_r[t] = r;
+    if (threadIdx.x == 0) {                             // visible after cluster_min's barriers
+      sh_r[t] = r;
+      piv_mark[r >> 5] |= 1u << (r & 31);
+    }
     if (gtid == 0) {
       st->rs[t] = r;
       s.basis[r - 1] = (int)k;
@@ -533,10 +582,8 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
     }
     ++it;
     r_prev = r;
-    best = block_min(best);
-    if (tid == 0) s.pcand[blockIdx.x] = best;
-    cluster_barrier();
-    best = fold_cands(s.pcand, G);
+    best = cluster_min(best, slot, ph);
+    ph ^= 1;
   }
   if (gtid == 0) {
     st->status = status;
@@ -627,6 +674,40 @@ __global__ void __launch_bounds__(kThreads + 32) k_update_s(SlabView s, int nc, 
     const int k = n % K;
     mbar_wait(&full[k], (n / K) & 1);
     const int rin = min(R, nr - n * R);
+    if (se == S && rin == R && act) {
+      // full block, full stage: the R rows' 2R chains interleave (independent FMAs)
+      double2 v[R];
+      const double2* cc2[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        v[rr] = *reinterpret_cast<const double2*>(sT + ((size_t)k * R + rr) * cw + jl);
+        cc2[rr] = reinterpret_cast<const double2*>(sC + ((size_t)k * R + rr) * kMaxLook);
+      }
+#pragma unroll
+      for (int h = 0; h < S / 2; ++h) {
+        double2 a[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) a[rr] = cc2[rr][h];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          v[rr].x = __fma_rn(-a[rr].x, pr[2 * h].x, v[rr].x);
+          v[rr].y = __fma_rn(-a[rr].x, pr[2 * h].y, v[rr].y);
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          v[rr].x = __fma_rn(-a[rr].y, pr[2 * h + 1].x, v[rr].x);
+          v[rr].y = __fma_rn(-a[rr].y, pr[2 * h + 1].y, v[rr].y);
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        const int i = g + (n * R + rr) * Gr;
+        if (!((mark[i >> 5] >> (i & 31)) & 1u)) *reinterpret_cast<double2*>(s.T + (long long)i * ld + j) = v[rr];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[k]);
+      continue;
+    }
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       if (rr < rin && act) {
@@ -792,10 +873,11 @@ cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cu
   return launch_ex(k_update<kUpdateRows>, grid, kThreads, 0, st, pdl, s, q, tol_opt);
 }
 
-static cudaLaunchConfig_t lookahead_config(int cluster, cudaStream_t st, cudaLaunchAttribute* attr) {
+static cudaLaunchConfig_t lookahead_config(int cluster, size_t smem, cudaStream_t st, cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cluster);
   cfg.blockDim = dim3(kLookThreads);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cluster;
@@ -811,7 +893,7 @@ int lookahead_cluster_size() {
   cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   for (int c : {16, 8, 4, 2, 1}) {
     cudaLaunchAttribute attr[1];
-    cudaLaunchConfig_t cfg = lookahead_config(c, nullptr, attr);
+    cudaLaunchConfig_t cfg = lookahead_config(c, 4096, nullptr, attr);
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, k_lookahead, &cfg) == cudaSuccess && n >= 1) return c;
     cudaGetLastError();
@@ -821,19 +903,19 @@ int lookahead_cluster_size() {
 
 cudaError_t launch_lookahead(const SlabView& s, int S, double tol_opt, double tol_piv, int cluster, cudaStream_t st) {
   cudaLaunchAttribute attr[1];
-  cudaLaunchConfig_t cfg = lookahead_config(cluster, st, attr);
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((s.rows + 31) / 32) * sizeof(unsigned int), st, attr);
   return cudaLaunchKernelEx(&cfg, k_lookahead, s, S, tol_opt, tol_piv);
 }
 
 // k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
 // SIMPLEX_PASS_CFG selects one for experiments (default 0).
 struct PassCfg { int R, K; };
-static const PassCfg kPassCfgs[] = {{2, 6}, {4, 4}, {1, 8}, {2, 8}};
+static const PassCfg kPassCfgs[] = {{2, 8}, {4, 4}, {1, 8}, {2, 6}, {2, 12}, {4, 6}};
 static int pass_cfg() {
   static int c = [] {
     const char* e = std::getenv("SIMPLEX_PASS_CFG");
     const int v = e ? std::atoi(e) : 0;
-    return (v >= 0 && v < 4) ? v : 0;
+    return (v >= 0 && v < 6) ? v : 0;
   }();
   return c;
 }
@@ -865,8 +947,10 @@ cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem) {
   switch (pass_cfg()) {
     case 1: return pass_prepare_s<4, 4>(S, smem, blocks_per_sm);
     case 2: return pass_prepare_s<1, 8>(S, smem, blocks_per_sm);
-    case 3: return pass_prepare_s<2, 8>(S, smem, blocks_per_sm);
-    default: return pass_prepare_s<2, 6>(S, smem, blocks_per_sm);
+    case 3: return pass_prepare_s<2, 6>(S, smem, blocks_per_sm);
+    case 4: return pass_prepare_s<2, 12>(S, smem, blocks_per_sm);
+    case 5: return pass_prepare_s<4, 6>(S, smem, blocks_per_sm);
+    default: return pass_prepare_s<2, 8>(S, smem, blocks_per_sm);
   }
 }
 
@@ -886,8 +970,10 @@ cudaError_t launch_update_s(const SlabView& s, int S, int nc, int Gr, int cw, cu
   switch (pass_cfg()) {
     case 1: return pass_launch<4, 4>(s, S, nc, Gr, cw, smem, st, pdl);
     case 2: return pass_launch<1, 8>(s, S, nc, Gr, cw, smem, st, pdl);
-    case 3: return pass_launch<2, 8>(s, S, nc, Gr, cw, smem, st, pdl);
-    default: return pass_launch<2, 6>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 3: return pass_launch<2, 6>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 4: return pass_launch<2, 12>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 5: return pass_launch<4, 6>(s, S, nc, Gr, cw, smem, st, pdl);
+    default: return pass_launch<2, 8>(s, S, nc, Gr, cw, smem, st, pdl);
   }
 }
 
