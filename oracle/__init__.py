@@ -65,6 +65,14 @@ def lib():
                                C.POINTER(C.c_int32), C.POINTER(C.c_int32), i64,
                                dp, dp, dp, ip, C.POINTER(C.c_int), dp, ip]
         L.or_solve.restype = C.c_int
+        L.or_price_bland.argtypes = [dp, i64, C.c_double]
+        L.or_price_bland.restype = i64
+        L.or_ratio_bland.argtypes = [i64, i64, dp, i64, C.c_double, ip, dp]
+        L.or_ratio_bland.restype = i64
+        L.or_solve_rule.argtypes = [i64, i64, dp, dp, dp, C.c_double, C.c_double, i64, i64, C.c_int,
+                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32), i64,
+                                    dp, dp, dp, ip, C.POINTER(C.c_int), dp, ip]
+        L.or_solve_rule.restype = C.c_int
         L.or_brute_force.argtypes = [i64, i64, dp, dp, dp, C.c_double, dp, dp]
         L.or_brute_force.restype = C.c_int
         _lib = L
@@ -115,6 +123,22 @@ def ratio(T, k, tol_piv=TOL_PIV):
     return int(r), q.value
 
 
+def price_bland(row0, tol_opt=TOL_OPT):
+    """Bland's entering rule: first j with T[0][j] < -tol_opt, or -1."""
+    row0 = _f64(row0)
+    return int(lib().or_price_bland(_dp(row0), row0.size, tol_opt))
+
+
+def ratio_bland(T, k, basis, tol_piv=TOL_PIV):
+    """Bland's leaving rule: min ratio, exact ties -> smallest basic-variable index."""
+    T = _f64(T)
+    basis = np.ascontiguousarray(basis, dtype=np.int64)
+    q = C.c_double()
+    r = lib().or_ratio_bland(T.shape[0] - 1, T.shape[1], _dp(T), k, tol_piv,
+                             basis.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(q))
+    return int(r), q.value
+
+
 def pivot(T, r, k):
     """Step 3, in place on a C-contiguous float64 tableau."""
     assert T.dtype == np.float64 and T.flags.c_contiguous
@@ -155,9 +179,12 @@ class Result:
         return list(zip(self.trace_k.tolist(), self.trace_r.tolist()))
 
 
+DANTZIG, BLAND = 0, 1
+
+
 def solve(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, stop_after=-1,
-          trace_cap=None, keep_tableau=False) -> Result:
-    """Run the oracle (§III Steps Init/1/2/3/Iterate)."""
+          trace_cap=None, keep_tableau=False, rule=DANTZIG) -> Result:
+    """Run the oracle (§III Steps Init/1/2/3/Iterate); rule DANTZIG or BLAND."""
     A, b, c = _f64(A), _f64(b), _f64(c)
     m, n = A.shape
     if trace_cap is None:
@@ -170,7 +197,7 @@ def solve(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, stop_after
     obj, piv, st = C.c_double(), C.c_int64(), C.c_int()
     T = np.empty((m + 1, n + m + 1)) if keep_tableau else None
     basis = np.empty(m, dtype=np.int64) if keep_tableau else None
-    err = lib().or_solve(m, n, _dp(A), _dp(b), _dp(c), tol_opt, tol_piv, max_pivots, stop_after,
+    err = lib().or_solve_rule(m, n, _dp(A), _dp(b), _dp(c), tol_opt, tol_piv, max_pivots, stop_after, rule,
                          tk.ctypes.data_as(C.POINTER(C.c_int32)),
                          tr.ctypes.data_as(C.POINTER(C.c_int32)), trace_cap,
                          _dp(x), _dp(y), C.byref(obj), C.byref(piv), C.byref(st),

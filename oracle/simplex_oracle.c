@@ -16,6 +16,7 @@
  *   or_pivot    Step 3, pivoting
  *   or_solve    Iterate/Finalization
  *   or_extract  read x, y, objective off the final tableau
+ *   or_price_bland / or_ratio_bland / or_solve_rule  Bland's rule
  *   or_brute_force  vertex enumeration (independent check)
  *
  * Every point where the paper is silent takes the reading in SURVEY.md §8(c)
@@ -113,6 +114,35 @@ int64_t or_ratio(int64_t m, int64_t W, const double *T, int64_t k, double tol_pi
     return r;
 }
 
+/* Bland's rule (NEXT #3 of SURVEY.md §8(f); "Bland's rule: enter the
+ * lowest-index negative reduced cost (anti-cycling)").  Entering: the FIRST j (ascending)
+ * with T[0][j] < -tol_opt. */
+int64_t or_price_bland(const double *row0, int64_t len, double tol_opt)
+{
+    for (int64_t j = 0; j < len; j++)
+        if (row0[j] < -tol_opt) return j;
+    return -1;
+}
+
+/* Bland's leaving rule (Bland 1977): among rows with the minimum ratio (exact ties), the
+ * row whose BASIC VARIABLE has the smallest index (basis[i-1]); reading c4 does not apply
+ * under this rule.  Same eligibility (c5) and division (c8) as or_ratio. */
+int64_t or_ratio_bland(int64_t m, int64_t W, const double *T, int64_t k, double tol_piv,
+                       const int64_t *basis, double *q_out)
+{
+    int64_t r = -1;
+    double best = INFINITY;
+    for (int64_t i = 1; i <= m; i++) {
+        const double a = T[i * W + k];
+        if (a > tol_piv) {
+            const double q = T[i * W + (W - 1)] / a;
+            if (r == -1 || q < best || (q == best && basis[i - 1] < basis[r - 1])) { best = q; r = i; }
+        }
+    }
+    if (q_out) *q_out = best;
+    return r;
+}
+
 /* Step 3: "form the new simplex tableau ... by applying pivoting in
  * the rows of the previous tableau, using the new pivot row".  Gauss-Jordan with
  * the arithmetic of reading c8. col[] snapshots column k before it is overwritten;
@@ -152,11 +182,12 @@ void or_extract(int64_t m, int64_t n, const double *T, const int64_t *basis,
  * many pivots are done (prefix runs).  T_out (optional, (m+1)*W) receives the final
  * tableau; trace_k/trace_r (optional, capacity trace_cap) receive (k, r) per pivot
  * (k 0-based column, r 1-based row). */
-int or_solve(int64_t m, int64_t n, const double *A, const double *b, const double *c,
-             double tol_opt, double tol_piv, int64_t max_pivots, int64_t stop_after,
-             int32_t *trace_k, int32_t *trace_r, int64_t trace_cap,
-             double *x, double *y, double *obj, int64_t *pivots_out, int *status_out,
-             double *T_out, int64_t *basis_out)
+/* rule 0: Dantzig (readings c1-c4); rule 1: Bland (or_price_bland / or_ratio_bland). */
+int or_solve_rule(int64_t m, int64_t n, const double *A, const double *b, const double *c,
+                  double tol_opt, double tol_piv, int64_t max_pivots, int64_t stop_after, int rule,
+                  int32_t *trace_k, int32_t *trace_r, int64_t trace_cap,
+                  double *x, double *y, double *obj, int64_t *pivots_out, int *status_out,
+                  double *T_out, int64_t *basis_out)
 {
     const int64_t W = n + m + 1;
     double *T = T_out ? T_out : (double *)malloc(sizeof(double) * (size_t)((m + 1) * W));
@@ -179,9 +210,11 @@ int or_solve(int64_t m, int64_t n, const double *A, const double *b, const doubl
     int status = OR_RUNNING;
     for (;;) {
         if (stop_after >= 0 && it == stop_after) { status = OR_RUNNING; break; }
-        const int64_t k = or_price(T, n + m, tol_opt, NULL);              /* Step 1 */
+        const int64_t k = rule == 1 ? or_price_bland(T, n + m, tol_opt)  /* Step 1 */
+                                    : or_price(T, n + m, tol_opt, NULL);
         if (k < 0) { status = OR_OPTIMAL; break; }
-        const int64_t r = or_ratio(m, W, T, k, tol_piv, NULL);            /* Step 2 */
+        const int64_t r = rule == 1 ? or_ratio_bland(m, W, T, k, tol_piv, basis, NULL)  /* Step 2 */
+                                    : or_ratio(m, W, T, k, tol_piv, NULL);
         if (r < 0) { status = OR_UNBOUNDED; break; }
         if (it == cap) { status = OR_ITERATION_LIMIT; break; }
         or_pivot(m, W, T, r, k, col, prow);                                /* Step 3 */
@@ -196,6 +229,16 @@ int or_solve(int64_t m, int64_t n, const double *A, const double *b, const doubl
     if (!T_out) free(T);
     free(basis); free(col); free(prow);
     return OR_OK;
+}
+
+int or_solve(int64_t m, int64_t n, const double *A, const double *b, const double *c,
+             double tol_opt, double tol_piv, int64_t max_pivots, int64_t stop_after,
+             int32_t *trace_k, int32_t *trace_r, int64_t trace_cap,
+             double *x, double *y, double *obj, int64_t *pivots_out, int *status_out,
+             double *T_out, int64_t *basis_out)
+{
+    return or_solve_rule(m, n, A, b, c, tol_opt, tol_piv, max_pivots, stop_after, 0, trace_k, trace_r,
+                         trace_cap, x, y, obj, pivots_out, status_out, T_out, basis_out);
 }
 
 /* ---- independent check: brute-force vertex enumeration ----

@@ -349,3 +349,66 @@ def test_certificate_flags_counterexamples():
     bad_x = res.x.copy()
     bad_x[0] += 1.0
     assert oracle.certificate(A, b, c, bad_x, res.y).violations
+
+
+# ---------------------------------------------------------------- Bland's rule (NEXT #3)
+def test_bland_steps_by_definition():
+    # entering: FIRST index with T[0][j] < -tol, not the most negative
+    assert oracle.price_bland(arr([0.0, -1.0, -5.0])) == 1
+    assert oracle.price_bland(arr([0.0, 0.5, 1e-9])) == -1
+    # leaving: exact ratio tie (3 = 3/1 = 6/2) -> smallest BASIC-VARIABLE index, not lowest row
+    T = _tab_from_col([1.0, 2.0], [3.0, 6.0])
+    assert oracle.ratio_bland(T, 0, basis=[7, 4])[0] == 2
+    assert oracle.ratio_bland(T, 0, basis=[4, 7])[0] == 1
+    assert oracle.ratio_bland(_tab_from_col([-1.0, 0.0], [1.0, 1.0]), 0, basis=[1, 2])[0] == -1
+
+
+def test_bland_terminates_on_beale():
+    # the cycling instance terminates OPTIMAL under Bland, at the true
+    # optimum 1/20 (brute force), where Dantzig + lowest-row ties cycles to the cap
+    A, b, c = F.beale()
+    res = oracle.solve(A, b, c, rule=oracle.BLAND)
+    assert res.status == oracle.OPTIMAL
+    found, bf, xb = oracle.brute_force(A, b, c)
+    assert abs(res.objective - bf) <= 1e-12 and abs(bf - 0.05) < 1e-12
+    assert np.allclose(res.x, [0.04, 0.0, 1.0, 0.0], atol=1e-12)
+    assert oracle.solve(A, b, c).status == oracle.ITERATION_LIMIT
+
+
+def test_bland_brute_force_and_certificates():
+    # degenerate, tie-heavy tiny LPs: Bland always terminates at the brute-force optimum
+    for A, b, c in _tiny_cases():
+        res = oracle.solve(A, b, c, rule=oracle.BLAND)
+        assert res.status == oracle.OPTIMAL
+        found, bf, _ = oracle.brute_force(A, b, c)
+        assert abs(res.objective - bf) <= 1e-9 * max(1.0, abs(bf))
+        assert not oracle.certificate(A, b, c, res.x, res.y).violations
+
+
+def test_bland_invariants_every_pivot():
+    rng = np.random.default_rng(8)
+    for _ in range(10):
+        m, n = int(rng.integers(3, 25)), int(rng.integers(3, 25))
+        A, b, c = F.tie_heavy(m, n, int(rng.integers(1 << 30)))
+        A[:, A.sum(axis=0) == 0] = 1.0
+        T, basis = oracle.build_tableau(A, b, c)
+        prev = T[0, -1]
+        for _it in range(20 * (m + n)):
+            k = oracle.price_bland(T[0, :-1])
+            if k < 0:
+                break
+            r, q = oracle.ratio_bland(T, k, basis)
+            assert r > 0
+            oracle.pivot(T, r, k)
+            basis[r - 1] = k
+            for i in range(1, m + 1):
+                e = np.zeros(m + 1)
+                e[i] = 1.0
+                assert np.array_equal(T[:, basis[i - 1]], e)
+            assert T[0, -1] >= prev
+            prev = T[0, -1]
+        else:
+            raise AssertionError("Bland's rule did not terminate")
+        # the stepwise run and or_solve_rule agree
+        res = oracle.solve(A, b, c, rule=oracle.BLAND, keep_tableau=True)
+        assert np.array_equal(res.T, T)
