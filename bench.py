@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--lookahead", type=int, default=0,
                     help="pivots per tableau pass (0: library default = 16 on one column part, 1 with "
                          "N > 1; 1: one pass per pivot; 2..16: rank-s look-ahead)")
+    ap.add_argument("--pivot-rule", default="dantzig", choices=["dantzig", "bland"],
+                    help="entering/leaving rule (bland = SURVEY.md §8(f) NEXT #3)")
     ap.add_argument("--single-pass-pivots", type=int, default=1000,
                     help="pivots of the one-pivot-per-pass k_update roofline window (0: skip)")
     return ap.parse_args()
@@ -222,7 +224,8 @@ def main():
     dy = torch.empty(m, dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
 
-    solver = sx.Simplex(dA, db, dc, group=group, lookahead=args.lookahead)
+    rule = sx.BLAND if args.pivot_rule == "bland" else sx.DANTZIG
+    solver = sx.Simplex(dA, db, dc, group=group, lookahead=args.lookahead, pivot_rule=rule)
     st = solver.stats()
     tableau_bytes = 8 * (m + 1) * (n + m + 1)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -246,6 +249,8 @@ def main():
     status, obj, piv = one_step(reload=False)
     parity = {"checked": False}
     gpath = os.path.join(ROOT, "tests", "golden", f"dense_{m}x{n}_s{args.seed}.npz")
+    if args.pivot_rule != "dantzig":
+        gpath = gpath[:-4] + f"_{args.pivot_rule}.npz"
     k, r = solver.trace()
     if os.path.exists(gpath):
         g = np.load(gpath)
@@ -291,7 +296,7 @@ def main():
     # (event-record nodes in the captured graph, on the stream the kernel runs on).  Kept
     # out of the value steps because an event node between two pivot kernels disables the
     # programmatic-dependent-launch edge the production loop uses.
-    prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead)
+    prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule)
     barrier()
     window = min(piv, args.roofline_pivots)
     prof.iterate(window)
@@ -310,7 +315,7 @@ def main():
     # ---- the one-pivot-per-pass kernel (k_update) measured the same way, for reference
     single = None
     if look > 1 and args.single_pass_pivots > 0:
-        p1 = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=1)
+        p1 = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=1, pivot_rule=rule)
         barrier()
         p1.iterate(min(piv, args.single_pass_pivots))
         barrier()
@@ -356,8 +361,9 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (lpgen SplitMix64 dense LP seed {args.seed}: A,c~U[1,10), b~U[n,2n); "
                     "SPEC.md:365-380 recipe)",
-            "config": {"workload": f"dense random LP m={m} n={n} FP64 seed {args.seed}, slack basis, Dantzig "
-                                   "+ lowest-index ties", "m": m, "n": n, "pivots_per_solve": piv,
+            "config": {"workload": f"dense random LP m={m} n={n} FP64 seed {args.seed}, slack basis, "
+                                   + ("Dantzig + lowest-index ties" if args.pivot_rule == "dantzig" else
+                                      "Bland's rule"), "m": m, "n": n, "pivots_per_solve": piv,
                        "pivots_per_tableau_pass": look,
                        "time_to_solve_ms": total_ms / args.steps,
                        "parallelism": f"column slabs x{world}" + (" (NCCL allgather/pivot)" if world > 1 else ""),

@@ -93,6 +93,11 @@ typedef struct {
                                chained corrections, then ONE pass applies all s — bitwise
                                identical to s single pivots; one column part only);
                                0 (default) = 16 on one column part, else 1                 */
+    int32_t  pivot_rule;    /* 0 = Dantzig (default): most negative T[0][j], lowest j / lowest
+                               row on ties (readings c1-c4); 1 = Bland: first j
+                               with T[0][j] < -tol_opt, ratio ties -> smallest basic-variable
+                               index (anti-cycling)   */
+    int32_t  reserved;
 } simplex_options;
 
 typedef struct {

@@ -27,6 +27,7 @@ ERR_NAME = {E_ARG: "SIMPLEX_E_ARG", E_NONFINITE: "SIMPLEX_E_NONFINITE", E_NEG_RH
             E_OOM: "SIMPLEX_E_OOM", E_CUDA: "SIMPLEX_E_CUDA", E_NCCL: "SIMPLEX_E_NCCL",
             E_STATE: "SIMPLEX_E_STATE"}
 RUNNING, OPTIMAL, UNBOUNDED, INFEASIBLE, ITERATION_LIMIT = -1, 0, 2, 3, 4
+DANTZIG, BLAND = 0, 1
 STATUS_NAME = {RUNNING: "RUNNING", OPTIMAL: "OPTIMAL", UNBOUNDED: "UNBOUNDED",
                INFEASIBLE: "INFEASIBLE", ITERATION_LIMIT: "ITERATION_LIMIT"}
 
@@ -42,7 +43,8 @@ class Options(C.Structure):
                 ("max_pivots", C.c_int64), ("record_trace", C.c_int32), ("device", C.c_int32),
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_void_p),
                 ("stream", C.c_void_p), ("virtual_ranks", C.c_int32), ("segment_pivots", C.c_int32),
-                ("time_kernels", C.c_int32), ("lookahead", C.c_int32)]
+                ("time_kernels", C.c_int32), ("lookahead", C.c_int32),
+                ("pivot_rule", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -170,7 +172,7 @@ class Simplex:
 
     def __init__(self, A, b, c, *, tol_opt=1e-7, tol_piv=1e-10, max_pivots=0, record_trace=True,
                  device=None, group=None, virtual_ranks=1, segment_pivots=0, time_kernels=False,
-                 lookahead=0, stream=None):
+                 lookahead=0, pivot_rule=DANTZIG, stream=None):
         L = lib()
         m, n = (int(A.shape[0]), int(A.shape[1]))
         o = default_options()
@@ -181,6 +183,7 @@ class Simplex:
         o.segment_pivots = int(segment_pivots)
         o.time_kernels = 1 if time_kernels else 0
         o.lookahead = int(lookahead)
+        o.pivot_rule = int(pivot_rule)
         s = stream if stream is not None else _current_stream()
         o.stream = s if s else None
         self._idbuf = None

@@ -59,6 +59,7 @@ struct SlabView {
   int rows;            // m + 1
   int w;               // local non-rhs columns; rhs is local column w
   long long c0;        // global index of local column 0
+  int rule;            // 0 Dantzig, 1 Bland (pivot_rule)
   int nslot;           // pricing slots: warps of 32 double2 of row 0 = ceil(ld/64)
   Cand* price;         // [nslot]
   double* col;         // [rows + 2]

@@ -217,6 +217,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
     v.c0 = c0;
     v.w = (int)w;
     v.rows = (int)(m + 1);
+    v.rule = opt.pivot_rule;
     v.ld = roundup(v.w + 1, 16);
     v.nslot = (int)((v.ld / 2 + 31) / 32);
     sl.sel_grid = (int)std::min<long long>((v.rows + sx::kThreads - 1) / sx::kThreads, 2LL * sms);
@@ -491,6 +492,7 @@ void simplex_default_options(simplex_options* o) {
   o->segment_pivots = 0;
   o->time_kernels = 0;
   o->lookahead = 0;
+  o->pivot_rule = 0;
 }
 
 simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* A, const double* b,
@@ -507,6 +509,7 @@ simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* 
     o = *opt;
   }
   if (!(o.tol_opt >= 0.0) || !(o.tol_piv >= 0.0)) return fail(SIMPLEX_E_ARG, "tolerances must be >= 0");
+  if (o.pivot_rule != 0 && o.pivot_rule != 1) return fail(SIMPLEX_E_ARG, "pivot_rule must be 0 (Dantzig) or 1 (Bland)");
   int prev = 0;
   cudaGetDevice(&prev);
   simplex_t* h = new simplex_s();

@@ -33,6 +33,17 @@ __device__ __forceinline__ bool cand_less(const Cand& a, const Cand& b) {
 }
 __device__ __forceinline__ Cand cand_min(const Cand& a, const Cand& b) { return cand_less(b, a) ? b : a; }
 
+// Step-1 candidate of column j with reduced cost v < -tol_opt: Dantzig keys on (v, j);
+// Bland keys on j alone (value 0), so the argmin is the first eligible column.
+__device__ __forceinline__ Cand price_cand(int rule, double v, long long j) { return Cand{rule ? 0.0 : v, j}; }
+
+// Step-2 candidate of row i with ratio q: Dantzig ties -> lowest row (reading c4); Bland
+// ties -> smallest basic-variable index (basis[i-1] in the high bits; row in the low 32).
+__device__ __forceinline__ Cand ratio_cand(int rule, double q, long long i, int basic) {
+  return Cand{q, rule ? (((long long)basic << 32) | i) : i};
+}
+__device__ __forceinline__ int cand_row(long long idx) { return (int)(idx & 0xffffffffLL); }
+
 __device__ __forceinline__ Cand warp_min(Cand c) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -187,8 +198,8 @@ __global__ void __launch_bounds__(kThreads) k_price0(SlabView s, double tol_opt)
   if (t < half) {
     const long long j = 2 * t;
     const double2 v = *reinterpret_cast<const double2*>(s.T + j);
-    if (j < s.w && v.x < -tol_opt) best = Cand{v.x, s.c0 + j};
-    if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, Cand{v.y, s.c0 + j + 1});
+    if (j < s.w && v.x < -tol_opt) best = price_cand(s.rule, v.x, s.c0 + j);
+    if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, price_cand(s.rule, v.y, s.c0 + j + 1));
   }
   best = warp_min(best);
   if ((threadIdx.x & 31) == 0) s.price[t >> 5] = best;
@@ -279,7 +290,8 @@ __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double
         rhs = s.T[i * s.ld + s.w];
       }
       s.col[i] = a;
-      if (i >= 1 && a > tol_piv) rbest = cand_min(rbest, Cand{__ddiv_rn(rhs, a), i});
+      if (i >= 1 && a > tol_piv)
+        rbest = cand_min(rbest, ratio_cand(s.rule, __ddiv_rn(rhs, a), i, s.rule ? s.basis[i - 1] : 0));
     }
   }
   rbest = block_min(rbest);
@@ -308,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double
       st->status = kIterLimit;
     } else {
       go = 1;
-      rr = (int)r.idx;
+      rr = cand_row(r.idx);
       st->r = rr;
       st->k = (int)k;
       st->p = __ldcg(s.col + rr);
@@ -372,8 +384,8 @@ __global__ void __launch_bounds__(kThreads) k_update(SlabView s, int q, double t
     v.y = __fma_rn(a, pr.y, v.y);
     if (k0 != r) *reinterpret_cast<double2*>(Tj + (long long)k0 * ld) = v;
     if (k0 == 0) {
-      if (j < s.w && v.x < -tol_opt) best = Cand{v.x, s.c0 + j};
-      if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, Cand{v.y, s.c0 + j + 1});
+      if (j < s.w && v.x < -tol_opt) best = price_cand(s.rule, v.x, s.c0 + j);
+      if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, price_cand(s.rule, v.y, s.c0 + j + 1));
     }
   }
   if ((t & ~31LL) < half) {                        // warp-uniform: warps holding row-0 lanes
@@ -493,7 +505,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
   for (long long j = gtid; j < ld; j += gthreads) {
     const double v = T[j];
     R0[j] = v;
-    if (j < w && v < -tol_opt) best = cand_min(best, Cand{v, s.c0 + j});
+    if (j < w && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
   }
   for (long long i = gtid; i < rows; i += gthreads) RHS[i] = T[i * ld + w];
   best = cluster_min(best, slot, ph);
@@ -529,7 +541,8 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
           if (u < t) x = __fma_rn(-cu[u], pk[u], x);
       }
       colS[i * kMaxLook + t] = x;
-      if (i >= 1 && x > tol_piv) rb = cand_min(rb, Cand{__ddiv_rn(h, x), i});   // Step 2
+      if (i >= 1 && x > tol_piv)                                              // Step 2
+        rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
     }
     rb = cluster_min(rb, slot, ph);
     ph ^= 1;
@@ -539,7 +552,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
       break;
     }
     if (it >= cap) { status = kIterLimit; break; }                            // reading c12
-    const int r = (int)rb.idx;
+    const int r = cand_row(rb.idx);
     // ---- phase B: columns (pivot row of T^t, normalized; objective row of T^{t+1})
     double cr[kMaxLook];                                // col_u[r], u < t (L2, same for all columns)
 #pragma unroll
@@ -566,7 +579,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
       prow[j] = pj;
       const double v = __fma_rn(a0, pj, r0);
       R0[j] = v;
-      if (j < w && v < -tol_opt) best = cand_min(best, Cand{v, s.c0 + j});   // Step 1 of t+1
+      if (j < w && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));   // Step 1 of t+1
     }
     if (threadIdx.x == 0) {                             // visible after cluster_min's barriers
       sh_r[t] = r;
