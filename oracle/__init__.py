@@ -23,8 +23,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "simplex_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-RUNNING, OPTIMAL, UNBOUNDED, ITERATION_LIMIT = -1, 0, 2, 4
-STATUS_NAME = {RUNNING: "RUNNING", OPTIMAL: "OPTIMAL", UNBOUNDED: "UNBOUNDED",
+RUNNING, OPTIMAL, UNBOUNDED, INFEASIBLE, ITERATION_LIMIT = -1, 0, 2, 3, 4
+STATUS_NAME = {RUNNING: "RUNNING", OPTIMAL: "OPTIMAL", UNBOUNDED: "UNBOUNDED", INFEASIBLE: "INFEASIBLE",
                ITERATION_LIMIT: "ITERATION_LIMIT"}
 E_ARG, E_NONFINITE, E_NEG_RHS, E_OOM = -1, -2, -3, -4
 
@@ -73,6 +73,10 @@ def lib():
                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32), i64,
                                     dp, dp, dp, ip, C.POINTER(C.c_int), dp, ip]
         L.or_solve_rule.restype = C.c_int
+        L.or_solve_2phase.argtypes = [i64, i64, dp, dp, dp, C.c_double, C.c_double, i64, C.c_int,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), i64,
+                                      dp, dp, dp, ip, C.POINTER(C.c_int), ip]
+        L.or_solve_2phase.restype = C.c_int
         L.or_brute_force.argtypes = [i64, i64, dp, dp, dp, C.c_double, dp, dp]
         L.or_brute_force.restype = C.c_int
         _lib = L
@@ -207,6 +211,30 @@ def solve(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, stop_after
     npiv = piv.value
     keep = min(npiv, trace_cap)
     return Result(st.value, npiv, obj.value, x, y, tk[:keep].copy(), tr[:keep].copy(), T, basis)
+
+
+def solve_2phase(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, rule=DANTZIG,
+                 trace_cap=None):
+    """Two-phase method: b may have negative entries.
+    Returns a Result (no tableau) with .phase1_pivots."""
+    A, b, c = _f64(A), _f64(b), _f64(c)
+    m, n = A.shape
+    if trace_cap is None:
+        trace_cap = max_pivots if max_pivots > 0 else 20 * (m + n)
+    tk = np.zeros(max(trace_cap, 1), dtype=np.int32)
+    tr = np.zeros(max(trace_cap, 1), dtype=np.int32)
+    x, y = np.empty(n), np.empty(m)
+    obj, piv, st, p1 = C.c_double(), C.c_int64(), C.c_int(), C.c_int64(-1)
+    err = lib().or_solve_2phase(m, n, _dp(A), _dp(b), _dp(c), tol_opt, tol_piv, max_pivots, rule,
+                                tk.ctypes.data_as(C.POINTER(C.c_int32)),
+                                tr.ctypes.data_as(C.POINTER(C.c_int32)), trace_cap,
+                                _dp(x), _dp(y), C.byref(obj), C.byref(piv), C.byref(st), C.byref(p1))
+    if err:
+        raise OracleError(err)
+    keep = min(piv.value, trace_cap)
+    res = Result(st.value, piv.value, obj.value, x, y, tk[:keep].copy(), tr[:keep].copy())
+    res.phase1_pivots = p1.value
+    return res
 
 
 def brute_force(A, b, c, feas_tol=1e-9):

@@ -17,6 +17,7 @@
  *   or_solve    Iterate/Finalization
  *   or_extract  read x, y, objective off the final tableau
  *   or_price_bland / or_ratio_bland / or_solve_rule  Bland's rule
+ *   or_solve_2phase  Phase I + Phase II for b with negative entries (NEXT #2)
  *   or_brute_force  vertex enumeration (independent check)
  *
  * Every point where the paper is silent takes the reading in SURVEY.md §8(c)
@@ -48,6 +49,7 @@
 #define OR_RUNNING (-1)
 #define OR_OPTIMAL 0
 #define OR_UNBOUNDED 2
+#define OR_INFEASIBLE 3
 #define OR_ITERATION_LIMIT 4
 
 #define OR_OK 0
@@ -239,6 +241,117 @@ int or_solve(int64_t m, int64_t n, const double *A, const double *b, const doubl
 {
     return or_solve_rule(m, n, A, b, c, tol_opt, tol_piv, max_pivots, stop_after, 0, trace_k, trace_r,
                          trace_cap, x, y, obj, pivots_out, status_out, T_out, basis_out);
+}
+
+/* ---- Phase I ("start having as a basis a feasible
+ * basic solution"; SPEC.md:70-78 phase_one) -------------------------------------------------
+ * Two-phase method, written step by step (readings p1-p6 in DESIGN.md):
+ *  p1 layout: W2 = n + m + a + 1 columns: structural, slacks, one artificial per row with
+ *     b_i < 0 (in ascending row order), rhs.  A row with b_i < 0 is negated exactly
+ *     (-a_i, -e_i, -b_i) and gets +1 in its artificial column; its artificial is basic,
+ *     every other row keeps its slack.
+ *  p2 Phase I objective: maximize -(sum of artificials): row 0 = +1 on the artificial
+ *     columns, then each artificial-basic row is subtracted from row 0 in ascending row
+ *     order (row0[j] = fma(-1, T[i][j], row0[j])), which zeroes the basic columns.
+ *  p3 Phase I runs the method itself (Steps 1-3, same rule, same cap counter) over all
+ *     non-rhs columns.  Infeasible iff its optimum T[0][W2-1] < -1e-7.
+ *  p4 drive-out: for each row i ascending whose basic variable is artificial, pivot on the
+ *     first column j < n+m with |T[i][j]| > tol_piv (Gauss-Jordan of Step 3, counted and
+ *     traced as a pivot); a row with none is redundant and keeps its artificial at zero.
+ *  p5 Phase II objective: row 0 = -c on the structural columns, 0 elsewhere; for each row i
+ *     ascending whose basic variable j is structural, row0[col] = fma(c_j, T[i][col],
+ *     row0[col]) (prices the basis out).  Artificial columns never enter again (pricing
+ *     over j < n+m only).
+ *  p6 Phase II continues with the same rule, tolerances and cap; extraction as or_extract
+ *     (y_i = T[0][n+i-1] holds for negated rows too: their slack column is -e_i). */
+int or_solve_2phase(int64_t m, int64_t n, const double *A, const double *b, const double *c,
+                    double tol_opt, double tol_piv, int64_t max_pivots, int rule,
+                    int32_t *trace_k, int32_t *trace_r, int64_t trace_cap,
+                    double *x, double *y, double *obj, int64_t *pivots_out, int *status_out,
+                    int64_t *phase1_pivots_out)
+{
+    if (m < 1 || n < 1) return OR_E_ARG;
+    for (int64_t i = 0; i < m * n; i++) if (!isfinite(A[i])) return OR_E_NONFINITE;
+    for (int64_t i = 0; i < m; i++) if (!isfinite(b[i])) return OR_E_NONFINITE;
+    for (int64_t j = 0; j < n; j++) if (!isfinite(c[j])) return OR_E_NONFINITE;
+    int64_t a = 0;
+    for (int64_t i = 0; i < m; i++) if (b[i] < 0.0) a++;
+    const int64_t W = n + m + a + 1, nm = n + m;
+    double *T = (double *)calloc((size_t)((m + 1) * W), sizeof(double));
+    int64_t *basis = (int64_t *)malloc(sizeof(int64_t) * (size_t)m);
+    double *col = (double *)malloc(sizeof(double) * (size_t)(m + 1));
+    double *prow = (double *)malloc(sizeof(double) * (size_t)W);
+    if (!T || !basis || !col || !prow) { free(T); free(basis); free(col); free(prow); return OR_E_OOM; }
+    /* p1 */
+    int64_t art = 0;
+    for (int64_t i = 1; i <= m; i++) {
+        double *row = T + i * W;
+        const int neg = b[i - 1] < 0.0;
+        for (int64_t j = 0; j < n; j++) row[j] = neg ? -A[(i - 1) * n + j] : A[(i - 1) * n + j];
+        row[n + i - 1] = neg ? -1.0 : 1.0;
+        row[W - 1] = neg ? -b[i - 1] : b[i - 1];
+        if (neg) { row[nm + art] = 1.0; basis[i - 1] = nm + art; art++; }
+        else basis[i - 1] = n + i - 1;
+    }
+    /* p2 */
+    for (int64_t q = 0; q < a; q++) T[nm + q] = 1.0;
+    for (int64_t i = 1; i <= m; i++)
+        if (basis[i - 1] >= nm)
+            for (int64_t j = 0; j < W; j++) T[j] = fma(-1.0, T[i * W + j], T[j]);
+    const int64_t cap = max_pivots > 0 ? max_pivots : 20 * (m + n);
+    int64_t it = 0;
+    int status = OR_RUNNING;
+    int64_t price_len = W - 1;                                   /* Phase I: every column */
+    for (int phase = 1; phase <= 2 && status == OR_RUNNING; phase++) {
+        for (;;) {                                               /* p3 / p6: Steps 1-3 */
+            const int64_t k = rule == 1 ? or_price_bland(T, price_len, tol_opt)
+                                        : or_price(T, price_len, tol_opt, NULL);
+            if (k < 0) break;
+            const int64_t r = rule == 1 ? or_ratio_bland(m, W, T, k, tol_piv, basis, NULL)
+                                        : or_ratio(m, W, T, k, tol_piv, NULL);
+            if (r < 0) { status = OR_UNBOUNDED; break; }
+            if (it == cap) { status = OR_ITERATION_LIMIT; break; }
+            or_pivot(m, W, T, r, k, col, prow);
+            basis[r - 1] = k;
+            if (trace_k && it < trace_cap) { trace_k[it] = (int32_t)k; trace_r[it] = (int32_t)r; }
+            it++;
+        }
+        if (status != OR_RUNNING) break;
+        if (phase == 2) { status = OR_OPTIMAL; break; }
+        if (phase1_pivots_out) *phase1_pivots_out = it;
+        if (T[W - 1] < -1e-7) { status = OR_INFEASIBLE; break; } /* p3 */
+        for (int64_t i = 1; i <= m; i++) {                       /* p4 */
+            if (basis[i - 1] < nm) continue;
+            int64_t j = -1;
+            for (int64_t q = 0; q < nm; q++) if (fabs(T[i * W + q]) > tol_piv) { j = q; break; }
+            if (j < 0) continue;
+            if (it == cap) { status = OR_ITERATION_LIMIT; break; }
+            or_pivot(m, W, T, i, j, col, prow);
+            basis[i - 1] = j;
+            if (trace_k && it < trace_cap) { trace_k[it] = (int32_t)j; trace_r[it] = (int32_t)i; }
+            it++;
+        }
+        if (status != OR_RUNNING) break;
+        for (int64_t j = 0; j < W; j++) T[j] = 0.0;              /* p5 */
+        for (int64_t j = 0; j < n; j++) T[j] = -c[j];
+        for (int64_t i = 1; i <= m; i++) {
+            const int64_t jb = basis[i - 1];
+            if (jb < n)
+                for (int64_t q = 0; q < W; q++) T[q] = fma(c[jb], T[i * W + q], T[q]);
+        }
+        price_len = nm;
+    }
+    /* extraction (or_extract with the W2 layout) */
+    if (x) {
+        for (int64_t j = 0; j < n; j++) x[j] = 0.0;
+        for (int64_t i = 1; i <= m; i++) if (basis[i - 1] < n) x[basis[i - 1]] = T[i * W + W - 1];
+    }
+    if (y) for (int64_t i = 1; i <= m; i++) y[i - 1] = T[n + i - 1];
+    if (obj) *obj = T[W - 1];
+    if (pivots_out) *pivots_out = it;
+    if (status_out) *status_out = status;
+    free(T); free(basis); free(col); free(prow);
+    return OR_OK;
 }
 
 /* ---- independent check: brute-force vertex enumeration ----
