@@ -8,7 +8,8 @@
  *        maximize c^T x   subject to   A x <= b,  x >= 0,      A is m x n (dense)
  *
  * started from the slack basis (Table I rows x_{n+1..n+m}; "start
- * having as a basis a feasible basic solution"), so b >= 0 is required.
+ * having as a basis a feasible basic solution") when b >= 0, and from a Phase I basis of
+ * artificial variables when some b_i < 0 (two-phase method, options.phase1).
  *
  * Per pivot, entirely on the device (no host round trip per pivot):
  *   Step 1  entering column k = argmin_j T[0][j] over T[0][j] < -tol_opt,
@@ -55,7 +56,7 @@ typedef enum {
     SIMPLEX_OK = 0,
     SIMPLEX_E_ARG = -1,        /* NULL pointer, m < 1, n < 1, bad option, shape mismatch   */
     SIMPLEX_E_NONFINITE = -2,  /* NaN or Inf in A, b or c                                   */
-    SIMPLEX_E_NEG_RHS = -3,    /* some b_i < 0: slack basis infeasible (no Phase I here)     */
+    SIMPLEX_E_NEG_RHS = -3,    /* some b_i < 0 with phase1 = 0, or on more than one part     */
     SIMPLEX_E_OOM = -4,        /* device or pinned host allocation failed                   */
     SIMPLEX_E_CUDA = -5,       /* CUDA runtime error, or no CUDA device                     */
     SIMPLEX_E_NCCL = -6,       /* NCCL error (multi-GPU)                                    */
@@ -66,7 +67,7 @@ typedef enum {
     SIMPLEX_RUNNING = -1,          /* no terminal status reached yet                       */
     SIMPLEX_OPTIMAL = 0,           /* no T[0][j] < -tol_opt                                 */
     SIMPLEX_UNBOUNDED = 2,         /* entering column has no T[i][k] > tol_piv              */
-    SIMPLEX_INFEASIBLE = 3,        /* reserved (Phase I is not part of this path)           */
+    SIMPLEX_INFEASIBLE = 3,        /* Phase I optimum < -1e-7: Ax <= b, x >= 0 is empty      */
     SIMPLEX_ITERATION_LIMIT = 4    /* max_pivots pivots done and another one was possible   */
 } simplex_status;                  /* numbering = SPEC.md:473 exit codes                    */
 
@@ -97,7 +98,10 @@ typedef struct {
                                row on ties (readings c1-c4); 1 = Bland: first j
                                with T[0][j] < -tol_opt, ratio ties -> smallest basic-variable
                                index (anti-cycling)   */
-    int32_t  reserved;
+    int32_t  phase1;        /* 1 (default): b with negative entries runs the two-phase method
+                               (artificials, Phase I objective, drive-out, Phase II; one
+                               column part) and may end INFEASIBLE;
+                               0: b_i < 0 is rejected with SIMPLEX_E_NEG_RHS               */
 } simplex_options;
 
 typedef struct {

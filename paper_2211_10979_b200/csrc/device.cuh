@@ -49,6 +49,8 @@ struct alignas(16) DevState {
   unsigned int err;    // build/validation error bits
   unsigned int ticket; // last-block ticket of k_select
   unsigned int ticket2;
+  int phase;           // 1: Phase I (artificials in the basis), 2: the problem's objective
+  int pw;              // columns priced (local): all non-rhs in Phase I, no artificials after
   int s_eff;           // look-ahead: pivots selected for the pending rank-s pass
   int rs[kMaxLook];    // look-ahead: their pivot rows, in order
 };
@@ -60,6 +62,10 @@ struct SlabView {
   int w;               // local non-rhs columns; rhs is local column w
   long long c0;        // global index of local column 0
   int rule;            // 0 Dantzig, 1 Bland (pivot_rule)
+  int arts;            // artificial columns (rows with b_i < 0), global columns n+m .. n+m+arts-1
+  int* art_of_row;     // [m] artificial index of row i+1, or -1
+  int* neg_rows;       // [arts] rows (1-based) with b_i < 0, ascending
+  double* cvec;        // [n] c, for the Phase II objective row
   int nslot;           // pricing slots: warps of 32 double2 of row 0 = ceil(ld/64)
   Cand* price;         // [nslot]
   double* col;         // [rows + 2]

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -88,7 +89,8 @@ struct simplex_s {
   cudaStream_t user_stream = nullptr;  // caller's stream (NULL = legacy default stream)
   cudaEvent_t ev_user = nullptr, ev_loop0 = nullptr, ev_loop1 = nullptr;
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
-  long long m = 0, n = 0, W = 0;
+  long long m = 0, n = 0, W = 0, arts = 0;   // arts: artificial columns (rows with b_i < 0)
+  std::vector<int> art_rows;               // rows with b_i < 0 at create (1-based)
   int nranks = 1, rank = 0, nslabs = 1, nparts = 1;
   simplex_options opt{};
   long long cap = 0;
@@ -116,6 +118,7 @@ struct simplex_s {
   std::vector<cudaEvent_t> tev[2];
   // host view of the loop
   int status = SIMPLEX_RUNNING;
+  int phase = 2;                    // 1 while the Phase I objective is being optimized
   long long it = 0;
   // stats
   long long graph_launches = 0, kernel_launches = 0, upd_launches = 0;
@@ -155,7 +158,9 @@ struct simplex_s {
     return SIMPLEX_OK;
   }
 
-  simplex_err setup(long long m_, long long n_, const simplex_options* o);
+  simplex_err setup(long long m_, long long n_, const double* b, const simplex_options* o);
+  simplex_err scan_b(const double* b, std::vector<int>* art_of_row, std::vector<int>* neg);
+  simplex_err phase_transition();
   simplex_err load(const double* A, const double* b, const double* c);
   simplex_err build_graphs();
   simplex_err enqueue_pivot(int slot, int t);
@@ -164,10 +169,28 @@ struct simplex_s {
   void release();
 };
 
-simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* o) {
+// Rows with b_i < 0 (1-based, ascending) and their artificial index (reading p1).
+simplex_err simplex_s::scan_b(const double* b, std::vector<int>* art_of_row, std::vector<int>* neg) {
+  std::vector<double> hb((size_t)m);
+  if (stream) {                                   // ordered after the caller's stream (enter())
+    CK(cudaMemcpyAsync(hb.data(), b, sizeof(double) * m, cudaMemcpyDefault, stream));
+    CK(cudaStreamSynchronize(stream));
+  } else {
+    CK(cudaMemcpy(hb.data(), b, sizeof(double) * m, cudaMemcpyDefault));
+  }
+  art_of_row->assign((size_t)m, -1);
+  neg->clear();
+  for (long long i = 0; i < m; ++i)
+    if (hb[i] < 0.0) {
+      (*art_of_row)[i] = (int)neg->size();
+      neg->push_back((int)(i + 1));
+    }
+  return SIMPLEX_OK;
+}
+
+simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const simplex_options* o) {
   m = m_;
   n = n_;
-  W = n + m + 1;
   opt = *o;
   nranks = std::max(1, opt.nranks);
   rank = opt.rank;
@@ -198,6 +221,15 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
   }
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  // Phase I (NEXT #2): one artificial column per row with b_i < 0
+  std::vector<int> art_of_row;
+  RET(scan_b(b, &art_of_row, &art_rows));
+  arts = (long long)art_rows.size();
+  W = n + m + arts + 1;
+  if (arts > 0 && (nparts > 1 || !opt.phase1))
+    return fail(SIMPLEX_E_NEG_RHS, nparts > 1 ? "b has negative entries: Phase I runs on one column part only"
+                                              : "b has a negative entry and phase1 = 0");
+
   user_stream = static_cast<cudaStream_t>(opt.stream);
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming));
@@ -213,11 +245,12 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
     Slab& sl = slabs[s];
     sx::SlabView& v = sl.v;
     int64_t c0 = 0, w = 0;
-    RET(simplex_partition(n + m, nparts, p, &c0, &w));
+    RET(simplex_partition(n + m + arts, nparts, p, &c0, &w));
     v.c0 = c0;
     v.w = (int)w;
     v.rows = (int)(m + 1);
     v.rule = opt.pivot_rule;
+    v.arts = (int)arts;
     v.ld = roundup(v.w + 1, 16);
     v.nslot = (int)((v.ld / 2 + 31) / 32);
     sl.sel_grid = (int)std::min<long long>((v.rows + sx::kThreads - 1) / sx::kThreads, 2LL * sms);
@@ -229,8 +262,10 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
       CK(sx::update_s_occupancy(look, &occ, sx::update_s_smem(sl.cw, v.rows)));
       if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
       sl.Gr = (int)std::max(1LL, std::min<long long>(v.rows, (long long)occ * sms / sl.nc));
-    } else {
-      // k_update: kUpdateCtasPerSm CTAs per SM; thread t owns column pair t mod (ld/2)
+    }
+    {
+      // k_update (one pivot per pass; also the Phase I drive-out pivots): kUpdateCtasPerSm
+      // CTAs per SM; thread t owns column pair t mod (ld/2)
       int occ = 1;
       CK(sx::update_occupancy(&occ));
       const long long tpr = v.ld / 2;                      // threads per row
@@ -250,6 +285,9 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
     }
     RET(dalloc(&v.rcand, std::max(sl.sel_grid, sl.look_grid)));
     RET(dalloc(&v.basis, m));
+    RET(dalloc(&v.art_of_row, m));
+    RET(dalloc(&v.neg_rows, std::max<long long>(arts, 1)));
+    RET(dalloc(&v.cvec, n));
     v.trace_cap = opt.record_trace ? cap : 0;
     RET(dalloc(&v.trace_k, std::max<long long>(v.trace_cap, 1)));
     RET(dalloc(&v.trace_r, std::max<long long>(v.trace_cap, 1)));
@@ -290,9 +328,17 @@ simplex_err simplex_s::setup(long long m_, long long n_, const simplex_options* 
 simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
   if (!A || !b || !c) return fail(SIMPLEX_E_ARG, "NULL input pointer");
   RET(enter());
+  std::vector<int> art_of_row, neg;
+  RET(scan_b(b, &art_of_row, &neg));
+  if ((long long)neg.size() != arts)
+    return fail(SIMPLEX_E_ARG, "reset: the number of negative b entries differs from create's");
+  art_rows = neg;
   CK(cudaMemcpyAsync(d_b, b, sizeof(double) * m, cudaMemcpyDefault, stream));
   for (auto& sl : slabs) {
     sx::SlabView& v = sl.v;
+    CK(cudaMemcpyAsync(v.art_of_row, art_of_row.data(), sizeof(int) * m, cudaMemcpyHostToDevice, stream));
+    if (arts > 0) CK(cudaMemcpyAsync(v.neg_rows, neg.data(), sizeof(int) * arts, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(v.cvec, c, sizeof(double) * n, cudaMemcpyDefault, stream));
     const long long ns = std::max<long long>(0, std::min<long long>(v.c0 + v.w, n) - v.c0);  // structural cols
     if (ns > 0) {
       // A's slab columns straight into rows 1..m (pitched copy), c's into row 0
@@ -302,9 +348,11 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
     }
     CK(sx::launch_init_state(v, n, cap, stream));
     CK(sx::launch_build(v, d_b, n, stream, sms));
+    if (arts > 0) CK(sx::launch_phase1_row0(v, stream));     // Phase I objective (reading p2)
     CK(sx::launch_price0(v, opt.tol_opt, stream));
   }
-  kernel_launches += 3 * nslabs;
+  CK(cudaStreamSynchronize(stream));                          // host vectors above go out of scope
+  kernel_launches += (3 + (arts > 0 ? 1 : 0)) * nslabs;
   // validation result
   unsigned int err = 0;
   for (int s = 0; s < nslabs; ++s) {
@@ -322,9 +370,9 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
     err = h_state[2].err;
   }
   status = SIMPLEX_RUNNING;
+  phase = arts > 0 ? 1 : 2;
   it = 0;
   if (err & sx::kErrNonFinite) return fail(SIMPLEX_E_NONFINITE, "A, b or c contains NaN or Inf");
-  if (err & sx::kErrNegRhs) return fail(SIMPLEX_E_NEG_RHS, "b has a negative entry: slack basis infeasible");
   return SIMPLEX_OK;
 }
 
@@ -407,36 +455,44 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
   for (auto& sl : slabs) CK(sx::launch_set_stop(sl.v.st, stop_at, stream));
   kernel_launches += nslabs;
   CK(cudaEventRecord(ev_loop0, stream));
-  long long launched = 0, completed = 0, seen = it;
-  bool stop = false;
   for (;;) {
-    while (!stop && launched - completed < 2) {
-      const int slot = (int)(launched & 1);
-      CK(cudaGraphLaunch(seg[slot], stream));
-      CK(cudaEventRecord(ev_done[slot], stream));
-      ++launched;
-      ++graph_launches;
-      kernel_launches += kernels_per_segment();
-    }
-    const int slot = (int)(completed & 1);
-    CK(cudaEventSynchronize(ev_done[slot]));
-    const sx::DevState hs = h_state[slot];
-    ++completed;
-    const long long piv = hs.it - seen;
-    if (opt.time_kernels) {
-      const long long passes = look > 1 ? (piv + look - 1) / look : piv;   // k_update launches that did work
-      for (long long q = 0; q < passes && q < steps_per_segment(); ++q) {
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, tev[slot][2 * q], tev[slot][2 * q + 1]));
-        upd_ms += ms;
-        ++upd_launches;
+    long long launched = 0, completed = 0, seen = it;
+    bool stop = false;
+    for (;;) {
+      while (!stop && launched - completed < 2) {
+        const int slot = (int)(launched & 1);
+        CK(cudaGraphLaunch(seg[slot], stream));
+        CK(cudaEventRecord(ev_done[slot], stream));
+        ++launched;
+        ++graph_launches;
+        kernel_launches += kernels_per_segment();
       }
+      const int slot = (int)(completed & 1);
+      CK(cudaEventSynchronize(ev_done[slot]));
+      const sx::DevState hs = h_state[slot];
+      ++completed;
+      const long long piv = hs.it - seen;
+      if (opt.time_kernels) {
+        const long long passes = look > 1 ? (piv + look - 1) / look : piv;   // k_update launches that did work
+        for (long long q = 0; q < passes && q < steps_per_segment(); ++q) {
+          float ms = 0.f;
+          CK(cudaEventElapsedTime(&ms, tev[slot][2 * q], tev[slot][2 * q + 1]));
+          upd_ms += ms;
+          ++upd_launches;
+        }
+      }
+      seen = hs.it;
+      status = hs.status;
+      it = hs.it;
+      if (hs.status != SIMPLEX_RUNNING || hs.it >= stop_at) stop = true;
+      if (stop && completed == launched) break;
     }
-    seen = hs.it;
-    status = hs.status;
-    it = hs.it;
-    if (hs.status != SIMPLEX_RUNNING || hs.it >= stop_at) stop = true;
-    if (stop && completed == launched) break;
+    // Phase I optimal: decide feasibility, drive artificials out, install the objective
+    if (status == SIMPLEX_OPTIMAL && phase == 1) {
+      RET(phase_transition());
+      if (status == SIMPLEX_RUNNING && it < stop_at) continue;
+    }
+    break;
   }
   CK(cudaEventRecord(ev_loop1, stream));
   CK(cudaEventSynchronize(ev_loop1));
@@ -444,6 +500,56 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
   CK(cudaEventElapsedTime(&ms, ev_loop0, ev_loop1));
   loop_ms += ms;
   if (done) *done = it - it0;
+  return SIMPLEX_OK;
+}
+
+// Phase I -> Phase II on one column part (readings p3-p5 of DESIGN.md), between device loops:
+// infeasible iff the Phase I optimum < -1e-7; each artificial still basic (rows ascending) is
+// pivoted out on its first column j < n+m with |T[i][j]| > tol_piv (a host-chosen pivot run
+// by the same update kernel); then the Phase II objective row is priced out on the device.
+simplex_err simplex_s::phase_transition() {
+  Slab& sl = slabs[0];
+  sx::SlabView& v = sl.v;
+  RET(flush_all());
+  std::vector<int> basis((size_t)m);
+  CK(cudaMemcpyAsync(&h_state[2].p, v.T + v.w, sizeof(double), cudaMemcpyDeviceToHost, stream));
+  CK(cudaMemcpyAsync(basis.data(), v.basis, sizeof(int) * m, cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  phase = 2;
+  if (h_state[2].p < -1e-7) {
+    status = SIMPLEX_INFEASIBLE;
+    CK(sx::launch_set_status(v.st, SIMPLEX_INFEASIBLE, stream));
+    CK(cudaStreamSynchronize(stream));
+    return SIMPLEX_OK;
+  }
+  std::vector<double> row((size_t)(n + m));
+  for (long long i = 1; i <= m; ++i) {
+    if (basis[i - 1] < n + m) continue;
+    CK(cudaMemcpyAsync(row.data(), v.T + i * v.ld, sizeof(double) * (n + m), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    long long j = -1;
+    for (long long q = 0; q < n + m; ++q)
+      if (std::fabs(row[q]) > opt.tol_piv) { j = q; break; }
+    if (j < 0) continue;                                  // redundant row: artificial stays at 0
+    if (it >= cap) {
+      status = SIMPLEX_ITERATION_LIMIT;
+      CK(sx::launch_set_status(v.st, SIMPLEX_ITERATION_LIMIT, stream));
+      CK(cudaStreamSynchronize(stream));
+      return SIMPLEX_OK;
+    }
+    CK(sx::launch_force(v, (int)i, (int)j, stream));
+    CK(sx::launch_update(v, sl.q, opt.tol_opt, sl.upd_grid, stream, false));
+    RET(flush_all());
+    kernel_launches += 2;
+    basis[i - 1] = (int)j;
+    ++it;
+  }
+  CK(sx::launch_phase2_row0(v, n, stream));
+  CK(sx::launch_price0(v, opt.tol_opt, stream));
+  CK(sx::launch_set_status(v.st, SIMPLEX_RUNNING, stream));
+  kernel_launches += 3;
+  CK(cudaStreamSynchronize(stream));
+  status = SIMPLEX_RUNNING;
   return SIMPLEX_OK;
 }
 
@@ -493,6 +599,7 @@ void simplex_default_options(simplex_options* o) {
   o->time_kernels = 0;
   o->lookahead = 0;
   o->pivot_rule = 0;
+  o->phase1 = 1;
 }
 
 simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* A, const double* b,
@@ -513,7 +620,7 @@ simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* 
   int prev = 0;
   cudaGetDevice(&prev);
   simplex_t* h = new simplex_s();
-  simplex_err e = h->setup(m, n, &o);
+  simplex_err e = h->setup(m, n, b, &o);
   if (e == SIMPLEX_OK) e = h->load(A, b, c);
   cudaSetDevice(prev);
   if (e != SIMPLEX_OK) {

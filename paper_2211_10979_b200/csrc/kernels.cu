@@ -128,14 +128,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // and c's slab columns into row 0.  Writes everything else of Table I and checks
 // finiteness / b >= 0.  One thread per (row, column pair).
 __global__ void __launch_bounds__(kThreads) k_build(SlabView s, const double* __restrict__ b, long long n) {
+  // Phase I layout (reading p1, NEXT #2): a row with b_i < 0 (art_of_row >= 0) is negated
+  // exactly and gets +1 in its artificial column n+m+art; row 0 is then the Phase I
+  // objective (+1 on the artificials) instead of -c.
   const long long halfld = s.ld >> 1;
   const long long total = (long long)s.rows * halfld;
+  const long long nm = n + (s.rows - 1);
   uint32_t err = 0;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long i = e / halfld;
     const long long j0 = (e - i * halfld) * 2;
     double* row = s.T + i * s.ld;
+    const int art = i >= 1 ? s.art_of_row[i - 1] : -1;
+    const bool neg = art >= 0;
 #pragma unroll
     for (int d = 0; d < 2; ++d) {
       const long long j = j0 + d;
@@ -149,14 +155,17 @@ __global__ void __launch_bounds__(kThreads) k_build(SlabView s, const double* __
         } else {
           v = b[i - 1];
           if (!isfinite(v)) err |= kErrNonFinite;
-          else if (v < 0.0) err |= kErrNegRhs;
+          if (neg) v = -v;
         }
       } else if (g < n) {                          // structural column: copied from A / c
         v = row[j];
         if (!isfinite(v)) err |= kErrNonFinite;
-        if (i == 0) v = -v;                        // row 0 stores -c
-      } else {                                     // slack column x_{g+1}: e_{g-n+1}
-        v = (i >= 1 && g - n == i - 1) ? 1.0 : 0.0;
+        if (i == 0) v = s.arts > 0 ? 0.0 : -v;     // row 0 stores -c
+        else if (neg) v = -v;
+      } else if (g < nm) {                         // slack column x_{g+1}: +-e_{g-n+1}
+        v = (i >= 1 && g - n == i - 1) ? (neg ? -1.0 : 1.0) : 0.0;
+      } else {                                     // artificial column g-nm
+        v = (i == 0 || art == (int)(g - nm)) ? 1.0 : 0.0;
       }
       row[j] = v;
     }
@@ -166,8 +175,10 @@ __global__ void __launch_bounds__(kThreads) k_build(SlabView s, const double* __
 
 __global__ void k_init_state(SlabView s, long long n, long long cap) {
   const int m = s.rows - 1;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-    s.basis[i] = (int)(n + i);                     // slack basis
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int art = s.art_of_row[i];               // slack basis; artificials
+    s.basis[i] = art >= 0 ? (int)(n + m + art) : (int)(n + i);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     DevState* st = s.st;
     st->it = 0;
@@ -183,8 +194,61 @@ __global__ void k_init_state(SlabView s, long long n, long long cap) {
     st->ticket = 0;
     st->ticket2 = 0;
     st->s_eff = 0;
+    st->phase = s.arts > 0 ? 1 : 2;
+    st->pw = s.w;                                  // Phase I prices every non-rhs column
   }
 }
+
+// Phase I objective (reading p2): subtract every artificial-basic row from row 0, in
+// ascending row order, one FMA per step (thread per column: the oracle's rounding order).
+__global__ void __launch_bounds__(kThreads) k_phase1_row0(SlabView s) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= s.ld) return;
+  double acc = s.T[j];
+  for (int q = 0; q < s.arts; ++q) acc = __fma_rn(-1.0, s.T[(long long)s.neg_rows[q] * s.ld + j], acc);
+  s.T[j] = acc;
+}
+
+// Phase II objective (reading p5): row 0 = -c on the structural columns, 0 elsewhere, then
+// for each row i ascending whose basic variable j is structural: row0 = fma(c_j, row_i, row0).
+__global__ void __launch_bounds__(kThreads) k_phase2_row0(SlabView s, long long n) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= s.ld) return;
+  const long long g = s.c0 + j;
+  double acc = (j < s.w && g < n) ? -s.cvec[g] : 0.0;
+  for (int i = 1; i < s.rows; ++i) {
+    const int jb = s.basis[i - 1];
+    if (jb < n) acc = __fma_rn(s.cvec[jb], s.T[(long long)i * s.ld + j], acc);
+  }
+  s.T[j] = acc;
+  if (j == 0) {
+    s.st->phase = 2;
+    s.st->pw = (int)(n + s.rows - 1 - s.c0 < s.w ? n + s.rows - 1 - s.c0 : s.w);   // no artificials
+  }
+}
+
+// Host-chosen pivot (Phase I drive-out, reading p4): stage column k, set the loop state so
+// k_update applies pivot (r, k) exactly like a selected one (trace, basis, counter).
+__global__ void __launch_bounds__(kThreads) k_force(SlabView s, int r, int k) {
+  DevState* st = s.st;
+  for (int i = threadIdx.x; i < s.rows; i += blockDim.x) s.col[i] = s.T[(long long)i * s.ld + k];
+  if (threadIdx.x == 0) {
+    const long long it = st->it;
+    st->r = r;
+    st->k = k;
+    st->p = s.T[(long long)r * s.ld + k];
+    st->go = 1;
+    st->pend_r = r;
+    s.basis[r - 1] = k;
+    if (it < s.trace_cap) {
+      s.trace_k[it] = k;
+      s.trace_r[it] = r;
+    }
+    st->it = it + 1;
+  }
+}
+
+__global__ void k_set_status(DevState* st, int status) { st->status = status; }
 
 // ------------------------------------------------------------------ a1: initial pricing
 // Row 0 is split into warp slots of 32 double2 (64 columns); slot w holds the argmin of
@@ -198,8 +262,9 @@ __global__ void __launch_bounds__(kThreads) k_price0(SlabView s, double tol_opt)
   if (t < half) {
     const long long j = 2 * t;
     const double2 v = *reinterpret_cast<const double2*>(s.T + j);
-    if (j < s.w && v.x < -tol_opt) best = price_cand(s.rule, v.x, s.c0 + j);
-    if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, price_cand(s.rule, v.y, s.c0 + j + 1));
+    const int pw = s.st->pw;
+    if (j < pw && v.x < -tol_opt) best = price_cand(s.rule, v.x, s.c0 + j);
+    if (j + 1 < pw && v.y < -tol_opt) best = cand_min(best, price_cand(s.rule, v.y, s.c0 + j + 1));
   }
   best = warp_min(best);
   if ((threadIdx.x & 31) == 0) s.price[t >> 5] = best;
@@ -384,8 +449,9 @@ __global__ void __launch_bounds__(kThreads) k_update(SlabView s, int q, double t
     v.y = __fma_rn(a, pr.y, v.y);
     if (k0 != r) *reinterpret_cast<double2*>(Tj + (long long)k0 * ld) = v;
     if (k0 == 0) {
-      if (j < s.w && v.x < -tol_opt) best = price_cand(s.rule, v.x, s.c0 + j);
-      if (j + 1 < s.w && v.y < -tol_opt) best = cand_min(best, price_cand(s.rule, v.y, s.c0 + j + 1));
+      const int pw = st->pw;
+      if (j < pw && v.x < -tol_opt) best = price_cand(s.rule, v.x, s.c0 + j);
+      if (j + 1 < pw && v.y < -tol_opt) best = cand_min(best, price_cand(s.rule, v.y, s.c0 + j + 1));
     }
   }
   if ((t & ~31LL) < half) {                        // warp-uniform: warps holding row-0 lanes
@@ -487,7 +553,8 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int rows = s.rows;
   const long long ld = s.ld;
-  const int w = s.w;
+  const int w = s.w;                                  // rhs column
+  const int pw = st->pw;                              // priced columns (Phase II: no artificials)
   const double* __restrict__ T = s.T;
   double* __restrict__ colS = s.colS;
   double* __restrict__ prowS = s.prowS;
@@ -505,7 +572,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
   for (long long j = gtid; j < ld; j += gthreads) {
     const double v = T[j];
     R0[j] = v;
-    if (j < w && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+    if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
   }
   for (long long i = gtid; i < rows; i += gthreads) RHS[i] = T[i * ld + w];
   best = cluster_min(best, slot, ph);
@@ -579,7 +646,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
       prow[j] = pj;
       const double v = __fma_rn(a0, pj, r0);
       R0[j] = v;
-      if (j < w && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));   // Step 1 of t+1
+      if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));  // Step 1 of t+1
     }
     if (threadIdx.x == 0) {                             // visible after cluster_min's barriers
       sh_r[t] = r;
@@ -788,7 +855,7 @@ __global__ void k_extract(SlabView s, long long n, double* x, double* y, double*
     } else {
       const long long jl = t - m;
       const long long g = s.c0 + jl;
-      if (y && g >= n) y[g - n] = s.T[jl];
+      if (y && g >= n && g < n + m) y[g - n] = s.T[jl];
     }
   }
   if (obj && blockIdx.x == 0 && threadIdx.x == 0) *obj = s.T[s.w];
@@ -988,6 +1055,26 @@ cudaError_t launch_update_s(const SlabView& s, int S, int nc, int Gr, int cw, cu
     case 5: return pass_launch<4, 6>(s, S, nc, Gr, cw, smem, st, pdl);
     default: return pass_launch<2, 8>(s, S, nc, Gr, cw, smem, st, pdl);
   }
+}
+
+cudaError_t launch_phase1_row0(const SlabView& s, cudaStream_t st) {
+  k_phase1_row0<<<(int)((s.ld + kThreads - 1) / kThreads), kThreads, 0, st>>>(s);
+  SX_CHECK_LAUNCH();
+}
+
+cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st) {
+  k_phase2_row0<<<(int)((s.ld + kThreads - 1) / kThreads), kThreads, 0, st>>>(s, n);
+  SX_CHECK_LAUNCH();
+}
+
+cudaError_t launch_force(const SlabView& s, int r, int k, cudaStream_t st) {
+  k_force<<<1, kThreads, 0, st>>>(s, r, k);
+  SX_CHECK_LAUNCH();
+}
+
+cudaError_t launch_set_status(DevState* d, int status, cudaStream_t st) {
+  k_set_status<<<1, 1, 0, st>>>(d, status);
+  SX_CHECK_LAUNCH();
 }
 
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st) {

@@ -24,6 +24,10 @@ int update_s_max(int S);
 size_t update_s_smem(int cw, int rows);
 cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem);
 cudaError_t launch_update_s(const SlabView& s, int S, int nc, int Gr, int cw, cudaStream_t st, bool pdl);
+cudaError_t launch_phase1_row0(const SlabView& s, cudaStream_t st);
+cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st);
+cudaError_t launch_force(const SlabView& s, int r, int k, cudaStream_t st);
+cudaError_t launch_set_status(DevState* d, int status, cudaStream_t st);
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st);
 cudaError_t launch_extract(const SlabView& s, long long n, double* x, double* y, double* obj, cudaStream_t st);
 cudaError_t launch_hash(const SlabView& s, long long Wg, int include_rhs, unsigned long long* out,

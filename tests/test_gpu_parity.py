@@ -183,7 +183,7 @@ def test_errors(sx):
         sx.Simplex(bad, b, c)
     assert e.value.code == sx.E_NONFINITE if hasattr(sx, "E_NONFINITE") else -2
     with pytest.raises(sx.SimplexError) as e:
-        sx.Simplex(A, -b, c)
+        sx.Simplex(A, -b, c, phase1=False)
     assert e.value.code == -3
     with pytest.raises(sx.SimplexError) as e:
         sx.Simplex(A, b, np.array([np.inf, 1.0]))
