@@ -256,12 +256,29 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     sl.sel_grid = (int)std::min<long long>((v.rows + sx::kThreads - 1) / sx::kThreads, 2LL * sms);
     if (look > 1) {
       // k_update_s: column chunks of cw doubles x row groups; all CTAs resident
-      sl.nc = (int)((v.ld + 2 * sx::kThreads - 1) / (2 * sx::kThreads));
-      sl.cw = (int)roundup((v.ld + sl.nc - 1) / sl.nc, 2);
+      // (nc, cw, Gr) minimising the busiest CTA's share cw * ceil(rows / Gr) over the
+      // occ * sms resident slots, chunks at least 3/4 of the consumer lanes wide (e.g.
+      // 37 chunks x 8 row groups = 296 CTAs at 8000^2 instead of 32 x 9 = 288)
+      const int cwmax = 2 * sx::kThreads;
       int occ = 1;
-      CK(sx::update_s_occupancy(look, &occ, sx::update_s_smem(sl.cw, v.rows)));
+      CK(sx::update_s_occupancy(look, &occ, sx::update_s_smem(cwmax, v.rows)));
       if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
-      sl.Gr = (int)std::max(1LL, std::min<long long>(v.rows, (long long)occ * sms / sl.nc));
+      const char* ps = getenv("SIMPLEX_PASS_SMS");          // experiment hook
+      const long long slots = (long long)occ * (ps ? atoi(ps) : sms);
+      const long long nc0 = (v.ld + cwmax - 1) / cwmax;
+      long long best = LLONG_MAX;
+      for (long long nc = nc0; nc <= std::max(nc0, std::min(slots, 4 * nc0)); ++nc) {
+        const long long cw = roundup((v.ld + nc - 1) / nc, 2);
+        if (cw > cwmax || (cw < cwmax * 3 / 4 && nc > nc0)) continue;   // keep >= 3/4 of the lanes busy
+        const long long gr = std::max(1LL, std::min<long long>(v.rows, slots / nc));
+        const long long cost = cw * ((v.rows + gr - 1) / gr);
+        if (cost < best) {
+          best = cost;
+          sl.nc = (int)nc;
+          sl.cw = (int)cw;
+          sl.Gr = (int)gr;
+        }
+      }
     }
     {
       // k_update (one pivot per pass; also the Phase I drive-out pivots): kUpdateCtasPerSm
@@ -791,3 +808,11 @@ simplex_err simplex_partition(int64_t total_cols, int64_t nparts, int64_t part, 
 const char* simplex_version(void) { return "libsimplex 0.1.0 (sm_100a, dense full-tableau simplex)"; }
 
 }  // extern "C"
+
+#ifdef SX_LOOK_PROFILE
+// Profiling builds only (SIMPLEX_BUILD_PROFILE=1): the last k_lookahead's phase time stamps.
+extern "C" simplex_err simplex_debug_lookahead_profile(uint64_t* out) {
+  CK(sx::lprof_read(reinterpret_cast<unsigned long long*>(out)));
+  return SIMPLEX_OK;
+}
+#endif

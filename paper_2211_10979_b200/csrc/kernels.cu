@@ -535,6 +535,24 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph) {
   return sh_res;
 }
 
+#ifdef SX_LOOK_PROFILE
+// debug builds only: %globaltimer stamps of CTA 0 / thread 0 per look-ahead step
+__device__ unsigned long long g_lprof[16 * (kMaxLook * 4 + 4)];
+#define SX_LPROF(slot)                                                   \
+  do {                                                                   \
+    if (threadIdx.x == 0 && blockIdx.x < 16) {                           \
+      unsigned long long t_;                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) :: "memory"); \
+      g_lprof[blockIdx.x * (kMaxLook * 4 + 4) + (slot)] = t_;            \
+    }                                                                    \
+  } while (0)
+cudaError_t lprof_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_lprof, sizeof(g_lprof));
+}
+#else
+#define SX_LPROF(slot)
+#endif
+
 // k_lookahead: one thread-block cluster (one CTA per SM) selecting up to S pivots.  Per pivot t:
 //   phase A (rows, grid-stride): RHS <- T^t's rhs (apply pivot t-1), column k of T^t by the
 //            chain from T^0, staged into colS[.][t], Step-2 candidates -> cluster argmin -> r;
@@ -584,6 +602,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
     if (status != kRunning || it >= stop) break;
     if (best.idx == LLONG_MAX) { status = kOptimal; break; }                 // Step 1: optimal
     const long long k = best.idx;
+    SX_LPROF(4 * t);
     // ---- phase A: rows
     double pk[kMaxLook];                                // prow_u[k], u < t (L2, same for all rows)
 #pragma unroll
@@ -611,7 +630,9 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
       if (i >= 1 && x > tol_piv)                                              // Step 2
         rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
     }
+    SX_LPROF(4 * t + 1);
     rb = cluster_min(rb, slot, ph);
+    SX_LPROF(4 * t + 2);
     ph ^= 1;
     if (rb.idx == LLONG_MAX) {                                                 // unbounded
       status = kUnbounded;
@@ -662,9 +683,14 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
     }
     ++it;
     r_prev = r;
+#ifdef SX_LOOK_PROFILE
+    __syncthreads();                                    // all warps of the CTA done with phase B
+#endif
+    SX_LPROF(4 * t + 3);
     best = cluster_min(best, slot, ph);
     ph ^= 1;
   }
+  SX_LPROF(4 * kMaxLook);
   if (gtid == 0) {
     st->status = status;
     st->it = it;
@@ -686,7 +712,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
 // stream (bitmap) but written at the end from their last normalized value prow_u, chained
 // over the later pivots of the block.
 template <int S, int R, int K>
-__global__ void __launch_bounds__(kThreads + 32) k_update_s(SlabView s, int nc, int Gr, int cw) {
+__global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int nc, int Gr, int cw) {
   pdl_launch_dependents();
   pdl_wait();
   const DevState* st = s.st;
@@ -763,11 +789,18 @@ __global__ void __launch_bounds__(kThreads + 32) k_update_s(SlabView s, int nc, 
         v[rr] = *reinterpret_cast<const double2*>(sT + ((size_t)k * R + rr) * cw + jl);
         cc2[rr] = reinterpret_cast<const double2*>(sC + ((size_t)k * R + rr) * kMaxLook);
       }
+      // the pivot-column entries are loaded one pair ahead of their FMAs (software
+      // pipeline: the shared-memory latency hides behind the previous pair's chains)
+      double2 ca[R][S / 2];
+#pragma unroll
+      for (int h = 0; h < S / 2; ++h)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) ca[rr][h] = cc2[rr][h];
 #pragma unroll
       for (int h = 0; h < S / 2; ++h) {
         double2 a[R];
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) a[rr] = cc2[rr][h];
+        for (int rr = 0; rr < R; ++rr) a[rr] = ca[rr][h];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
           v[rr].x = __fma_rn(-a[rr].x, pr[2 * h].x, v[rr].x);
@@ -990,7 +1023,7 @@ cudaError_t launch_lookahead(const SlabView& s, int S, double tol_opt, double to
 // k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
 // SIMPLEX_PASS_CFG selects one for experiments (default 0).
 struct PassCfg { int R, K; };
-static const PassCfg kPassCfgs[] = {{2, 8}, {4, 4}, {1, 8}, {2, 6}, {2, 12}, {4, 6}};
+static const PassCfg kPassCfgs[] = {{2, 8}, {4, 4}, {1, 8}, {1, 16}, {2, 10}, {3, 8}};
 static int pass_cfg() {
   static int c = [] {
     const char* e = std::getenv("SIMPLEX_PASS_CFG");
@@ -1027,9 +1060,9 @@ cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem) {
   switch (pass_cfg()) {
     case 1: return pass_prepare_s<4, 4>(S, smem, blocks_per_sm);
     case 2: return pass_prepare_s<1, 8>(S, smem, blocks_per_sm);
-    case 3: return pass_prepare_s<2, 6>(S, smem, blocks_per_sm);
-    case 4: return pass_prepare_s<2, 12>(S, smem, blocks_per_sm);
-    case 5: return pass_prepare_s<4, 6>(S, smem, blocks_per_sm);
+    case 3: return pass_prepare_s<1, 16>(S, smem, blocks_per_sm);
+    case 4: return pass_prepare_s<2, 10>(S, smem, blocks_per_sm);
+    case 5: return pass_prepare_s<3, 8>(S, smem, blocks_per_sm);
     default: return pass_prepare_s<2, 8>(S, smem, blocks_per_sm);
   }
 }
@@ -1050,9 +1083,9 @@ cudaError_t launch_update_s(const SlabView& s, int S, int nc, int Gr, int cw, cu
   switch (pass_cfg()) {
     case 1: return pass_launch<4, 4>(s, S, nc, Gr, cw, smem, st, pdl);
     case 2: return pass_launch<1, 8>(s, S, nc, Gr, cw, smem, st, pdl);
-    case 3: return pass_launch<2, 6>(s, S, nc, Gr, cw, smem, st, pdl);
-    case 4: return pass_launch<2, 12>(s, S, nc, Gr, cw, smem, st, pdl);
-    case 5: return pass_launch<4, 6>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 3: return pass_launch<1, 16>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 4: return pass_launch<2, 10>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 5: return pass_launch<3, 8>(s, S, nc, Gr, cw, smem, st, pdl);
     default: return pass_launch<2, 8>(s, S, nc, Gr, cw, smem, st, pdl);
   }
 }
