@@ -102,6 +102,11 @@ typedef struct {
                                (artificials, Phase I objective, drive-out, Phase II; one
                                column part) and may end INFEASIBLE;
                                0: b_i < 0 is rejected with SIMPLEX_E_NEG_RHS               */
+    int32_t  overlap;       /* rank-s look-ahead only.  1 (default): software pipeline —
+                               block b+1 is selected (on one thread-block cluster) WHILE
+                               block b's pass runs on the other SMs, out of place between
+                               two tableau buffers (2x the tableau's HBM); 0: select, then
+                               pass, in place.  Bitwise identical results either way.     */
 } simplex_options;
 
 typedef struct {

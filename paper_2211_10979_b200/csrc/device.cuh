@@ -21,7 +21,8 @@ constexpr int kIterLimit = 4;
 
 constexpr int kThreads = 256;              // threads per CTA for every kernel
 constexpr int kMaxLook = 16;               // max pivots per look-ahead block (rank-s update)
-constexpr int kLookThreads = 512;          // threads per CTA of the look-ahead selection (1 cluster)
+constexpr int kLookThreads = 256;          // threads per CTA of the look-ahead selection (1 cluster)
+constexpr int kColS = 2 * kMaxLook;        // colS row stride / prowS rows: two blocks (banks) of chains
 
 constexpr uint32_t kErrNonFinite = 1u;
 constexpr uint32_t kErrNegRhs = 2u;
@@ -51,8 +52,8 @@ struct alignas(16) DevState {
   unsigned int ticket2;
   int phase;           // 1: Phase I (artificials in the basis), 2: the problem's objective
   int pw;              // columns priced (local): all non-rhs in Phase I, no artificials after
-  int s_eff;           // look-ahead: pivots selected for the pending rank-s pass
-  int rs[kMaxLook];    // look-ahead: their pivot rows, in order
+  int sb[2];           // look-ahead: pivots selected into chain bank 0 / 1
+  int rsb[2][kMaxLook];// look-ahead: their pivot rows, in order
 };
 
 struct SlabView {
@@ -76,9 +77,10 @@ struct SlabView {
   int* trace_r;
   long long trace_cap;
   DevState* st;
-  // rank-s look-ahead (NEXT #1); NULL when the handle runs 1 pivot/pass
-  double* colS;        // [rows][kMaxLook]  pivot columns T^t[.][k_t], t-minor
-  double* prowS;       // [kMaxLook][ld]    normalized pivot rows T^t[r_t][.] / p_t
+  // rank-s look-ahead (NEXT #1); NULL when the handle runs 1 pivot/pass.
+  // Two banks of chains: bank q holds pivots u = 0..15 at colS[i][16q+u], prowS[16q+u][.]
+  double* colS;        // [rows][kColS]     pivot columns T^t[.][k_t], t-minor
+  double* prowS;       // [kColS][ld]       normalized pivot rows T^t[r_t][.] / p_t
   double* R0;          // [ld]              current objective row during selection
   double* RHS;         // [rows]            current rhs column during selection
   Cand* pcand;         // [look-ahead CTAs] Step-1 candidates per CTA

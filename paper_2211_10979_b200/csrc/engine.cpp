@@ -63,6 +63,7 @@ struct Slab {
   int sel_grid = 1;
   int look_grid = 0;     // look-ahead selection: CTAs of its single thread-block cluster
   int nc = 0, cw = 0, Gr = 0;   // rank-s pass: column chunks, chunk width, row groups
+  double* T2 = nullptr;          // second tableau buffer of the look-ahead software pipeline
 };
 
 class DeviceGuard {
@@ -111,6 +112,7 @@ struct simplex_s {
   // graph segments
   int S = 32;                       // pivots per captured graph segment
   int look = 1;                     // pivots per tableau pass (>1: rank-s look-ahead)
+  bool overlap = false;             // look-ahead software pipeline: select block b+1 during pass b
   bool pdl = true;                  // programmatic dependent launch between pivot kernels
   bool force_nccl = false;          // test hook: 1-rank NCCL exchange on one GPU
   bool graphs_ready = false;
@@ -148,7 +150,13 @@ struct simplex_s {
   bool gathered() const { return nparts > 1 || force_nccl; }
   bool use_nccl() const { return nranks > 1 || force_nccl; }
   int kernels_per_pivot() const { return nslabs * (2 + (gathered() ? 1 : 0)); }
-  int steps_per_segment() const { return look > 1 ? std::max(1, S / look) : S; }   // graph nodes
+  // graph steps per segment; the pipeline alternates two tableau buffers, so an even count
+  // brings the tableau back to buffer 0 at every segment boundary
+  int steps_per_segment() const {
+    if (look == 1) return S;
+    const int q = std::max(1, S / look);
+    return overlap ? (q + 1) / 2 * 2 : q;
+  }
   int kernels_per_segment() const { return look > 1 ? 2 * steps_per_segment() : S * kernels_per_pivot(); }
 
   simplex_err enter() {
@@ -209,6 +217,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   if (look > sx::kMaxLook) return fail(SIMPLEX_E_ARG, "lookahead larger than kMaxLook (16)");
   if (look > 1 && (nparts > 1 || force_nccl))
     return fail(SIMPLEX_E_ARG, "lookahead > 1 is implemented for one column part");
+  overlap = look > 1 && opt.overlap != 0;
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -255,16 +264,19 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     v.nslot = (int)((v.ld / 2 + 31) / 32);
     sl.sel_grid = (int)std::min<long long>((v.rows + sx::kThreads - 1) / sx::kThreads, 2LL * sms);
     if (look > 1) {
+      sl.look_grid = sx::lookahead_cluster_size();
+      if (sl.look_grid < 1) return fail(SIMPLEX_E_CUDA, "look-ahead selection cluster cannot be scheduled");
       // k_update_s: column chunks of cw doubles x row groups; all CTAs resident
       // (nc, cw, Gr) minimising the busiest CTA's share cw * ceil(rows / Gr) over the
-      // occ * sms resident slots, chunks at least 3/4 of the consumer lanes wide (e.g.
-      // 37 chunks x 8 row groups = 296 CTAs at 8000^2 instead of 32 x 9 = 288)
+      // occ * sms resident slots (pipelined: the SMs left over by the selection cluster),
+      // chunks at least 3/4 of the consumer lanes wide (e.g. 37 chunks x 8 row groups =
+      // 296 CTAs at 8000^2 instead of 32 x 9 = 288)
       const int cwmax = 2 * sx::kThreads;
       int occ = 1;
       CK(sx::update_s_occupancy(look, &occ, sx::update_s_smem(cwmax, v.rows)));
       if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
       const char* ps = getenv("SIMPLEX_PASS_SMS");          // experiment hook
-      const long long slots = (long long)occ * (ps ? atoi(ps) : sms);
+      const long long slots = (long long)occ * (ps ? atoi(ps) : overlap ? sms - sl.look_grid : sms);
       const long long nc0 = (v.ld + cwmax - 1) / cwmax;
       long long best = LLONG_MAX;
       for (long long nc = nc0; nc <= std::max(nc0, std::min(slots, 4 * nc0)); ++nc) {
@@ -296,10 +308,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     RET(dalloc(&v.price, v.nslot));
     RET(dalloc(&v.col, v.rows + 2));
     RET(dalloc(&v.rownorm, v.ld));
-    if (look > 1) {
-      sl.look_grid = sx::lookahead_cluster_size();
-      if (sl.look_grid < 1) return fail(SIMPLEX_E_CUDA, "look-ahead selection cluster cannot be scheduled");
-    }
+    if (overlap) RET(dalloc(&sl.T2, (size_t)v.rows * v.ld));
     RET(dalloc(&v.rcand, std::max(sl.sel_grid, sl.look_grid)));
     RET(dalloc(&v.basis, m));
     RET(dalloc(&v.art_of_row, m));
@@ -310,8 +319,8 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     RET(dalloc(&v.trace_r, std::max<long long>(v.trace_cap, 1)));
     RET(dalloc(&v.st, 1));
     if (look > 1) {
-      RET(dalloc(&v.colS, (size_t)v.rows * sx::kMaxLook));
-      RET(dalloc(&v.prowS, (size_t)sx::kMaxLook * v.ld));
+      RET(dalloc(&v.colS, (size_t)v.rows * sx::kColS));
+      RET(dalloc(&v.prowS, (size_t)sx::kColS * v.ld));
       RET(dalloc(&v.R0, v.ld));
       RET(dalloc(&v.RHS, v.rows));
       RET(dalloc(&v.pcand, sl.look_grid));
@@ -395,11 +404,32 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
 
 simplex_err simplex_s::enqueue_pivot(int slot, int t) {
   if (look > 1) {
-    // rank-s block: select up to `look` pivots ahead, then one pass applies them all
     const Slab& sl = slabs[0];
-    CK(sx::launch_lookahead(sl.v, look, opt.tol_opt, opt.tol_piv, sl.look_grid, stream));
+    if (overlap) {
+      // software pipeline: block t's starting tableau is in buffer t&1 and its
+      // pivots in chain bank t&1.  Select block t+1 (chaining block t first) into the other
+      // bank on the cluster, and let block t's pass (buffer t&1 -> the other) start on the
+      // remaining SMs as soon as the cluster is resident (PDL; it does not wait for it).
+      const int q = t & 1;
+      double* buf[2] = {sl.v.T, sl.T2};
+      static const bool time_sel = std::getenv("SIMPLEX_TIME_SELECT") != nullptr;   // experiment hook
+      if (opt.time_kernels && time_sel) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
+      CK(sx::launch_lookahead(sl.v, buf[q], look, q ^ 1, q, opt.tol_opt, opt.tol_piv, sl.look_grid, stream));
+      if (opt.time_kernels)
+        CK(cudaEventRecordWithFlags(tev[slot][2 * t + (time_sel ? 1 : 0)], stream, cudaEventRecordExternal));
+      if (opt.time_kernels && time_sel) {
+        CK(sx::launch_update_s(sl.v, look, buf[q], buf[q ^ 1], q, sl.nc, sl.Gr, sl.cw, stream, false));
+        return SIMPLEX_OK;
+      }
+      CK(sx::launch_update_s(sl.v, look, buf[q], buf[q ^ 1], q, sl.nc, sl.Gr, sl.cw, stream,
+                             pdl && !opt.time_kernels));
+      if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
+      return SIMPLEX_OK;
+    }
+    // rank-s block: select up to `look` pivots ahead, then one pass applies them all in place
+    CK(sx::launch_lookahead(sl.v, sl.v.T, look, 0, -1, opt.tol_opt, opt.tol_piv, sl.look_grid, stream));
     if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
-    CK(sx::launch_update_s(sl.v, look, sl.nc, sl.Gr, sl.cw, stream, pdl && !opt.time_kernels));
+    CK(sx::launch_update_s(sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, pdl && !opt.time_kernels));
     if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
     return SIMPLEX_OK;
   }
@@ -473,6 +503,12 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
   kernel_launches += nslabs;
   CK(cudaEventRecord(ev_loop0, stream));
   for (;;) {
+    if (overlap) {
+      // pipeline prologue: the first block is selected from the current tableau into bank 0
+      const Slab& sl = slabs[0];
+      CK(sx::launch_lookahead(sl.v, sl.v.T, look, 0, -1, opt.tol_opt, opt.tol_piv, sl.look_grid, stream));
+      ++kernel_launches;
+    }
     long long launched = 0, completed = 0, seen = it;
     bool stop = false;
     for (;;) {
@@ -503,6 +539,12 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
       it = hs.it;
       if (hs.status != SIMPLEX_RUNNING || hs.it >= stop_at) stop = true;
       if (stop && completed == launched) break;
+    }
+    if (overlap) {
+      // pipeline drain: the last selected block (bank 0) is applied in place to buffer 0
+      const Slab& sl = slabs[0];
+      CK(sx::launch_update_s(sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
+      ++kernel_launches;
     }
     // Phase I optimal: decide feasibility, drive artificials out, install the objective
     if (status == SIMPLEX_OPTIMAL && phase == 1) {
@@ -617,6 +659,7 @@ void simplex_default_options(simplex_options* o) {
   o->lookahead = 0;
   o->pivot_rule = 0;
   o->phase1 = 1;
+  o->overlap = 1;
 }
 
 simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* A, const double* b,

@@ -193,7 +193,8 @@ __global__ void k_init_state(SlabView s, long long n, long long cap) {
     st->err = 0;
     st->ticket = 0;
     st->ticket2 = 0;
-    st->s_eff = 0;
+    st->sb[0] = 0;
+    st->sb[1] = 0;
     st->phase = s.arts > 0 ? 1 : 2;
     st->pw = s.w;                                  // Phase I prices every non-rhs column
   }
@@ -536,13 +537,13 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph) {
 }
 
 #ifdef SX_LOOK_PROFILE
-// debug builds only: %globaltimer stamps of CTA 0 / thread 0 per look-ahead step
+// debug builds only: SM clock stamps (clock64: cheap, per-SM) of thread 0 per look-ahead step
 __device__ unsigned long long g_lprof[16 * (kMaxLook * 4 + 4)];
 #define SX_LPROF(slot)                                                   \
   do {                                                                   \
     if (threadIdx.x == 0 && blockIdx.x < 16) {                           \
       unsigned long long t_;                                             \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) :: "memory"); \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) :: "memory");     \
       g_lprof[blockIdx.x * (kMaxLook * 4 + 4) + (slot)] = t_;            \
     }                                                                    \
   } while (0)
@@ -553,80 +554,114 @@ cudaError_t lprof_read(unsigned long long* out) {
 #define SX_LPROF(slot)
 #endif
 
-// k_lookahead: one thread-block cluster (one CTA per SM) selecting up to S pivots.  Per pivot t:
-//   phase A (rows, grid-stride): RHS <- T^t's rhs (apply pivot t-1), column k of T^t by the
-//            chain from T^0, staged into colS[.][t], Step-2 candidates -> cluster argmin -> r;
-//   phase B (columns, grid-stride): row r of T^t by the chain, prowS[t] = row / p, the
-//            objective row R0 <- T^{t+1}'s, Step-1 candidates -> cluster argmin -> k of t+1.
+// k_lookahead: one thread-block cluster (one CTA per SM) selecting up to S pivots into chain
+// bank `bown`.  Per pivot t:
+//   phase A (rows, grid-stride): RHS <- the rhs after the previous pivot, column k of the
+//            current tableau by the chain from T, staged into colS[.][bown][t], Step-2
+//            candidates -> cluster argmin -> r;
+//   phase B (columns, grid-stride): row r by the chain, prowS[bown][t] = row / p, the
+//            objective row R0 <- the next one, Step-1 candidates -> cluster argmin -> k of t+1.
+// `T` is the tableau the chains start from.  bpre < 0 (prologue): T is the current tableau and
+// R0 / RHS are read from it.  bpre >= 0 (software pipeline): T is the tableau
+// BEFORE the previous block, whose pass is running concurrently on the other SMs; its pivots
+// (bank bpre) are chained first, R0 / RHS continue from the previous launch.  Chained in the
+// oracle's order, every value is bitwise the one the single-pivot sequence produces.
 // Every thread always owns the same rows / columns, so R0, RHS, colS[i][.] and prowS[.][j]
 // are only re-read by their writer; values written by OTHER CTAs are read with ld.cg.  All
 // loads a phase needs (per-step scalars, the T entry, the pending chain operands) are issued
 // before the first dependent use, so each phase costs about one memory latency.
-__global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, double tol_opt, double tol_piv) {
+__global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const double* __restrict__ T, int S,
+                                                           int bown, int bpre, double tol_opt, double tol_piv) {
+  pdl_launch_dependents();                            // the previous block's pass may start now
   DevState* st = s.st;
-  __shared__ int sh_r[kMaxLook];
+  __shared__ int sh_r[kMaxLook];                      // own pivot rows
+  __shared__ int sh_rp[kMaxLook];                     // pivot rows of the previous block (bpre)
   __shared__ __align__(16) Cand slot[2 * 16];
-  extern __shared__ unsigned int piv_mark[];          // rows already pivot rows in this block
+  extern __shared__ unsigned int piv_mark[];          // rows that are pivot rows of a pending chain
   const long long gthreads = (long long)gridDim.x * blockDim.x;
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int rows = s.rows;
   const long long ld = s.ld;
   const int w = s.w;                                  // rhs column
   const int pw = st->pw;                              // priced columns (Phase II: no artificials)
-  const double* __restrict__ T = s.T;
-  double* __restrict__ colS = s.colS;
-  double* __restrict__ prowS = s.prowS;
+  double* __restrict__ colO = s.colS + bown * kMaxLook;                 // row stride kColS
+  const double* __restrict__ colP = s.colS + (bpre >= 0 ? bpre : 0) * kMaxLook;
+  double* __restrict__ prowO = s.prowS + (long long)bown * kMaxLook * ld;
+  const double* __restrict__ prowP = s.prowS + (long long)(bpre >= 0 ? bpre : 0) * kMaxLook * ld;
   double* __restrict__ R0 = s.R0;
   double* __restrict__ RHS = s.RHS;
   long long it = st->it;
   int status = st->status;
   const long long stop = st->stop_at;
   const long long cap = st->cap;
+  const int spre = bpre >= 0 ? st->sb[bpre] : 0;
   int ph = 0;
   for (int q = threadIdx.x; q < (rows + 31) / 32; q += blockDim.x) piv_mark[q] = 0u;
+  if (threadIdx.x < kMaxLook) sh_rp[threadIdx.x] = (int)threadIdx.x < spre ? st->rsb[bpre][threadIdx.x] : -1;
+  __syncthreads();
+  if ((int)threadIdx.x < spre) atomicOr(&piv_mark[sh_rp[threadIdx.x] >> 5], 1u << (sh_rp[threadIdx.x] & 31));
 
-  // T^0's objective row and rhs column; Step 1 of the first pivot
+  // Step 1 of the first pivot, from T's objective row (prologue) or the running R0
   Cand best = cand_none();
-  for (long long j = gtid; j < ld; j += gthreads) {
-    const double v = T[j];
-    R0[j] = v;
-    if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+  if (bpre < 0) {
+    for (long long j = gtid; j < ld; j += gthreads) {
+      const double v = T[j];
+      R0[j] = v;
+      if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+    }
+    for (long long i = gtid; i < rows; i += gthreads) RHS[i] = T[i * ld + w];
+  } else {
+    for (long long j = gtid; j < pw; j += gthreads) {
+      const double v = R0[j];
+      if (v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+    }
   }
-  for (long long i = gtid; i < rows; i += gthreads) RHS[i] = T[i * ld + w];
-  best = cluster_min(best, slot, ph);
+  best = cluster_min(best, slot, ph);                 // (its barriers also publish piv_mark)
   ph ^= 1;
 
   int t = 0;
-  int r_prev = -1;
+  int r_prev = spre > 0 ? sh_rp[spre - 1] : -1;       // pivot not yet applied to RHS
+  const double* c_prev = spre > 0 ? colP + spre - 1 : nullptr;
+  const double* p_prev = spre > 0 ? prowP + (long long)(spre - 1) * ld : nullptr;
   for (; t < S; ++t) {
     if (status != kRunning || it >= stop) break;
     if (best.idx == LLONG_MAX) { status = kOptimal; break; }                 // Step 1: optimal
     const long long k = best.idx;
     SX_LPROF(4 * t);
     // ---- phase A: rows
-    double pk[kMaxLook];                                // prow_u[k], u < t (L2, same for all rows)
+    double qk[kMaxLook], pk[kMaxLook];                  // prow_u[k] of both banks (L2, same for all rows)
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) pk[u] = u < t ? __ldcg(prowS + (long long)u * ld + k) : 0.0;
-    const double pw_prev = t > 0 ? __ldcg(prowS + (long long)(t - 1) * ld + w) : 0.0;
+    for (int u = 0; u < kMaxLook; ++u) qk[u] = u < spre ? __ldcg(prowP + (long long)u * ld + k) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) pk[u] = u < t ? __ldcg(prowO + (long long)u * ld + k) : 0.0;
+    const double pw_prev = r_prev >= 0 ? __ldcg(p_prev + w) : 0.0;
     Cand rb = cand_none();
     for (long long i = gtid; i < rows; i += gthreads) {
       double x = T[i * ld + k];
       double h = RHS[i];
-      double cu[kMaxLook];                              // this row's pending-column entries
+      double cq[kMaxLook], cu[kMaxLook];                // this row's pending-column entries
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) cu[u] = u < t ? colS[i * kMaxLook + u] : 0.0;
-      if (t > 0) h = (i == r_prev) ? pw_prev : __fma_rn(-colS[i * kMaxLook + t - 1], pw_prev, h);
+      for (int u = 0; u < kMaxLook; ++u) cq[u] = u < spre ? colP[i * kColS + u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u) cu[u] = u < t ? colO[i * kColS + u] : 0.0;
+      if (r_prev >= 0) h = (i == r_prev) ? pw_prev : __fma_rn(-c_prev[i * kColS], pw_prev, h);
       RHS[i] = h;
-      if ((piv_mark[i >> 5] >> (i & 31)) & 1u) {       // row i was a pivot row of this block
+      if ((piv_mark[i >> 5] >> (i & 31)) & 1u) {       // row i is a pivot row of a pending chain
+#pragma unroll
+        for (int u = 0; u < kMaxLook; ++u)
+          if (u < spre) x = (i == sh_rp[u]) ? qk[u] : __fma_rn(-cq[u], qk[u], x);
 #pragma unroll
         for (int u = 0; u < kMaxLook; ++u)
           if (u < t) x = (i == sh_r[u]) ? pk[u] : __fma_rn(-cu[u], pk[u], x);
       } else {
 #pragma unroll
         for (int u = 0; u < kMaxLook; ++u)
+          if (u < spre) x = __fma_rn(-cq[u], qk[u], x);
+#pragma unroll
+        for (int u = 0; u < kMaxLook; ++u)
           if (u < t) x = __fma_rn(-cu[u], pk[u], x);
       }
-      colS[i * kMaxLook + t] = x;
+      colO[i * kColS + t] = x;
       if (i >= 1 && x > tol_piv)                                              // Step 2
         rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
     }
@@ -641,25 +676,34 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
     }
     if (it >= cap) { status = kIterLimit; break; }                            // reading c12
     const int r = cand_row(rb.idx);
-    // ---- phase B: columns (pivot row of T^t, normalized; objective row of T^{t+1})
-    double cr[kMaxLook];                                // col_u[r], u < t (L2, same for all columns)
+    // ---- phase B: columns (pivot row, normalized; the next objective row)
+    double cr[kMaxLook], cs[kMaxLook];                  // col_u[r] of both banks (L2, same for all columns)
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? __ldcg(colS + (long long)r * kMaxLook + u) : 0.0;
-    const double p = __ldcg(colS + (long long)r * kMaxLook + t);
-    const double a0 = -__ldcg(colS + t);                                      // col_t[0]
+    for (int u = 0; u < kMaxLook; ++u) cs[u] = u < spre ? __ldcg(colP + (long long)r * kColS + u) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? __ldcg(colO + (long long)r * kColS + u) : 0.0;
+    const double p = __ldcg(colO + (long long)r * kColS + t);
+    const double a0 = -__ldcg(colO + t);                                      // col_t[0]
     const double* Tr = T + (long long)r * ld;
-    double* prow = prowS + (long long)t * ld;
-    unsigned int rmask = 0u;                            // bit u: r was already pivot row u
+    double* prow = prowO + (long long)t * ld;
+    unsigned int rmask = 0u, qmask = 0u;                // bit u: r was pivot row u (own / previous bank)
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u)
+    for (int u = 0; u < kMaxLook; ++u) {
       if (u < t && sh_r[u] == r) rmask |= 1u << u;
+      if (u < spre && sh_rp[u] == r) qmask |= 1u << u;
+    }
     best = cand_none();
     for (long long j = gtid; j < ld; j += gthreads) {
       double x = Tr[j];
       const double r0 = R0[j];
-      double pu[kMaxLook];                              // this column's pending-row entries
+      double qu[kMaxLook], pu[kMaxLook];                // this column's pending-row entries
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? prowS[(long long)u * ld + j] : 0.0;
+      for (int u = 0; u < kMaxLook; ++u) qu[u] = u < spre ? prowP[(long long)u * ld + j] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? prowO[(long long)u * ld + j] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u)
+        if (u < spre) x = ((qmask >> u) & 1u) ? qu[u] : __fma_rn(-cs[u], qu[u], x);
 #pragma unroll
       for (int u = 0; u < kMaxLook; ++u)
         if (u < t) x = ((rmask >> u) & 1u) ? pu[u] : __fma_rn(-cr[u], pu[u], x);
@@ -674,7 +718,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
       piv_mark[r >> 5] |= 1u << (r & 31);
     }
     if (gtid == 0) {
-      st->rs[t] = r;
+      st->rsb[bown][t] = r;
       s.basis[r - 1] = (int)k;
       if (it < s.trace_cap) {
         s.trace_k[it] = (int)k;
@@ -683,9 +727,8 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
     }
     ++it;
     r_prev = r;
-#ifdef SX_LOOK_PROFILE
-    __syncthreads();                                    // all warps of the CTA done with phase B
-#endif
+    c_prev = colO + t;
+    p_prev = prow;
     SX_LPROF(4 * t + 3);
     best = cluster_min(best, slot, ph);
     ph ^= 1;
@@ -694,7 +737,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
   if (gtid == 0) {
     st->status = status;
     st->it = it;
-    st->s_eff = t;
+    st->sb[bown] = t;
     st->go = t > 0;
     st->pend_r = -1;
   }
@@ -711,12 +754,19 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, int S, d
 // rounding), then store with 128-bit st.global.  The <= s pivot rows are not stored by the
 // stream (bitmap) but written at the end from their last normalized value prow_u, chained
 // over the later pivots of the block.
+//
+// src == dst: in place.  src != dst (software pipeline): reads the block's
+// starting tableau, writes the next buffer — also when the block is empty (a copy) — and does
+// NOT wait on the look-ahead kernel launched just before it (that one selects the NEXT block,
+// from src, concurrently); everything this pass reads was complete before that launch began.
 template <int S, int R, int K>
-__global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int nc, int Gr, int cw) {
+__global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const double* __restrict__ src,
+                                                               double* dst, int bank, int nc, int Gr, int cw) {
   pdl_launch_dependents();
-  pdl_wait();
+  if (src == dst) pdl_wait();
   const DevState* st = s.st;
-  if (!st->go) return;
+  const int se = st->sb[bank];
+  if (se == 0 && src == dst) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sT = reinterpret_cast<double*>(smem_raw);                 // [K][R][cw]
   double* sC = sT + (size_t)K * R * cw;                              // [K][R][kMaxLook]
@@ -726,12 +776,11 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int n
   __shared__ int sh_r[S];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int se = st->s_eff;
   const int rows = s.rows;
   const long long ld = s.ld;
   const int nwords = (rows + 31) >> 5;
   for (int i = tid; i < nwords; i += blockDim.x) mark[i] = 0u;
-  if (tid < S) sh_r[tid] = tid < se ? st->rs[tid] : -1;
+  if (tid < S) sh_r[tid] = tid < se ? st->rsb[bank][tid] : -1;
   if (tid == 0) {
     for (int k = 0; k < K; ++k) {
       mbar_init(&full[k], 1);
@@ -759,8 +808,8 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int n
         mbar_arrive_expect_tx(&full[k], (uint32_t)(rin * (jn + kMaxLook) * sizeof(double)));
         for (int rr = 0; rr < rin; ++rr) {
           const long long i = g + (long long)(n * R + rr) * Gr;
-          bulk_g2s(sT + ((size_t)k * R + rr) * cw, s.T + i * ld + j0, (uint32_t)(jn * sizeof(double)), &full[k]);
-          bulk_g2s(sC + ((size_t)k * R + rr) * kMaxLook, s.colS + i * kMaxLook,
+          bulk_g2s(sT + ((size_t)k * R + rr) * cw, src + i * ld + j0, (uint32_t)(jn * sizeof(double)), &full[k]);
+          bulk_g2s(sC + ((size_t)k * R + rr) * kMaxLook, s.colS + i * kColS + bank * kMaxLook,
                    (uint32_t)(kMaxLook * sizeof(double)), &full[k]);
         }
       }
@@ -774,7 +823,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int n
   double2 pr[S];
 #pragma unroll
   for (int u = 0; u < S; ++u)
-    pr[u] = (act && u < se) ? *reinterpret_cast<const double2*>(s.prowS + (long long)u * ld + j)
+    pr[u] = (act && u < se) ? *reinterpret_cast<const double2*>(s.prowS + (long long)(bank * kMaxLook + u) * ld + j)
                             : make_double2(0.0, 0.0);
   for (int n = 0; n < nst; ++n) {
     const int k = n % K;
@@ -815,7 +864,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int n
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         const int i = g + (n * R + rr) * Gr;
-        if (!((mark[i >> 5] >> (i & 31)) & 1u)) *reinterpret_cast<double2*>(s.T + (long long)i * ld + j) = v[rr];
+        if (!((mark[i >> 5] >> (i & 31)) & 1u)) *reinterpret_cast<double2*>(dst + (long long)i * ld + j) = v[rr];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[k]);
@@ -835,7 +884,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int n
             v.y = __fma_rn(a, pr[u].y, v.y);
           }
         }
-        if (!((mark[i >> 5] >> (i & 31)) & 1u)) *reinterpret_cast<double2*>(s.T + (long long)i * ld + j) = v;
+        if (!((mark[i >> 5] >> (i & 31)) & 1u)) *reinterpret_cast<double2*>(dst + (long long)i * ld + j) = v;
       }
     }
     __syncwarp();
@@ -853,7 +902,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int n
     for (int u2 = u + 1; u2 < se; ++u2) last &= (sh_r[u2] != r);
     if (!last) continue;
     double2 v = pr[u];
-    const double* cr = s.colS + (long long)r * kMaxLook;
+    const double* cr = s.colS + (long long)r * kColS + bank * kMaxLook;
 #pragma unroll
     for (int u2 = 0; u2 < S; ++u2) {
       if (u2 > u && u2 < se) {
@@ -862,7 +911,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, int n
         v.y = __fma_rn(a, pr[u2].y, v.y);
       }
     }
-    *reinterpret_cast<double2*>(s.T + (long long)r * ld + j) = v;
+    *reinterpret_cast<double2*>(dst + (long long)r * ld + j) = v;
   }
 }
 
@@ -1004,7 +1053,10 @@ static cudaLaunchConfig_t lookahead_config(int cluster, size_t smem, cudaStream_
 // Largest cluster (16, else 8, 4, 2, 1 CTAs) the device can co-schedule for k_lookahead.
 int lookahead_cluster_size() {
   cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  const char* e = std::getenv("SIMPLEX_LOOK_CLUSTER");   // experiment hook: cap the cluster size
+  const int cmax = e ? std::atoi(e) : 16;
   for (int c : {16, 8, 4, 2, 1}) {
+    if (c > cmax) continue;
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = lookahead_config(c, 4096, nullptr, attr);
     int n = 0;
@@ -1014,10 +1066,11 @@ int lookahead_cluster_size() {
   return 0;
 }
 
-cudaError_t launch_lookahead(const SlabView& s, int S, double tol_opt, double tol_piv, int cluster, cudaStream_t st) {
+cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
+                             double tol_piv, int cluster, cudaStream_t st) {
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((s.rows + 31) / 32) * sizeof(unsigned int), st, attr);
-  return cudaLaunchKernelEx(&cfg, k_lookahead, s, S, tol_opt, tol_piv);
+  return cudaLaunchKernelEx(&cfg, k_lookahead, s, T, S, bown, bpre, tol_opt, tol_piv);
 }
 
 // k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
@@ -1068,25 +1121,26 @@ cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem) {
 }
 
 template <int R, int K>
-static cudaError_t pass_launch(const SlabView& s, int S, int nc, int Gr, int cw, size_t smem, cudaStream_t st,
-                               bool pdl) {
+static cudaError_t pass_launch(const SlabView& s, int S, const double* src, double* dst, int bank, int nc, int Gr,
+                               int cw, size_t smem, cudaStream_t st, bool pdl) {
   const int grid = nc * Gr;
   switch (update_s_max(S)) {
-    case 4: return launch_ex(k_update_s<4, R, K>, grid, kThreads + 32, smem, st, pdl, s, nc, Gr, cw);
-    case 8: return launch_ex(k_update_s<8, R, K>, grid, kThreads + 32, smem, st, pdl, s, nc, Gr, cw);
-    default: return launch_ex(k_update_s<16, R, K>, grid, kThreads + 32, smem, st, pdl, s, nc, Gr, cw);
+    case 4: return launch_ex(k_update_s<4, R, K>, grid, kThreads + 32, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
+    case 8: return launch_ex(k_update_s<8, R, K>, grid, kThreads + 32, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
+    default: return launch_ex(k_update_s<16, R, K>, grid, kThreads + 32, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
   }
 }
 
-cudaError_t launch_update_s(const SlabView& s, int S, int nc, int Gr, int cw, cudaStream_t st, bool pdl) {
+cudaError_t launch_update_s(const SlabView& s, int S, const double* src, double* dst, int bank, int nc, int Gr,
+                            int cw, cudaStream_t st, bool pdl) {
   const size_t smem = update_s_smem(cw, s.rows);
   switch (pass_cfg()) {
-    case 1: return pass_launch<4, 4>(s, S, nc, Gr, cw, smem, st, pdl);
-    case 2: return pass_launch<1, 8>(s, S, nc, Gr, cw, smem, st, pdl);
-    case 3: return pass_launch<1, 16>(s, S, nc, Gr, cw, smem, st, pdl);
-    case 4: return pass_launch<2, 10>(s, S, nc, Gr, cw, smem, st, pdl);
-    case 5: return pass_launch<3, 8>(s, S, nc, Gr, cw, smem, st, pdl);
-    default: return pass_launch<2, 8>(s, S, nc, Gr, cw, smem, st, pdl);
+    case 1: return pass_launch<4, 4>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 2: return pass_launch<1, 8>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 3: return pass_launch<1, 16>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 4: return pass_launch<2, 10>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 5: return pass_launch<3, 8>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    default: return pass_launch<2, 8>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
   }
 }
 

@@ -18,12 +18,17 @@ cudaError_t launch_select(const SlabView& s, const XView& x, double tol_piv, int
                           bool pdl);
 cudaError_t update_occupancy(int* blocks_per_sm);
 cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st, bool pdl);
-cudaError_t launch_lookahead(const SlabView& s, int S, double tol_opt, double tol_piv, int cluster, cudaStream_t st);
+// k_lookahead: select up to S pivots into chain bank `bown`, chaining from T (bpre >= 0: first
+// the pending pivots of bank bpre, whose pass runs concurrently)
+cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
+                             double tol_piv, int cluster, cudaStream_t st);
 int lookahead_cluster_size();
 int update_s_max(int S);
 size_t update_s_smem(int cw, int rows);
 cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem);
-cudaError_t launch_update_s(const SlabView& s, int S, int nc, int Gr, int cw, cudaStream_t st, bool pdl);
+// k_update_s: apply the pivots of chain bank `bank` to src, writing dst (src == dst: in place)
+cudaError_t launch_update_s(const SlabView& s, int S, const double* src, double* dst, int bank, int nc, int Gr,
+                            int cw, cudaStream_t st, bool pdl);
 cudaError_t launch_phase1_row0(const SlabView& s, cudaStream_t st);
 cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st);
 cudaError_t launch_force(const SlabView& s, int r, int k, cudaStream_t st);

@@ -1,6 +1,8 @@
 """GPU parity of the rank-s look-ahead path: s pivots selected
 ahead from chained corrections, one tableau pass applies them.  The claim is BITWISE
-identity with s single pivots, so every check is exact equality with the oracle."""
+identity with s single pivots, so every check is exact equality with the oracle.  Every
+case runs both schedules: the software pipeline (block b+1 selected while block b's pass
+runs, two tableau buffers; the default) and select-then-pass in place (overlap=False)."""
 import os
 
 import numpy as np
@@ -23,10 +25,15 @@ def sx(cuda_device):
     return sx
 
 
+@pytest.fixture(params=[True, False], ids=["pipe", "serial"])
+def ov(request):
+    return request.param
+
+
 @pytest.mark.parametrize("look", LOOKS)
 @pytest.mark.parametrize("name", ["classic", "chvatal", "unbounded", "beale", "entering_tie", "ratio_tie",
                                   "zero_iteration"])
-def test_worked_examples(sx, name, look):
+def test_worked_examples(sx, name, look, ov):
     if name == "classic":
         A, b, c = F.classic()
     elif name == "chvatal":
@@ -39,53 +46,54 @@ def test_worked_examples(sx, name, look):
         g = GOLD[name]
         A, b, c = (np.array(g[k], float) for k in ("A", "b", "c"))
     o = oracle.solve(A, b, c, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, lookahead=look), o)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=look, overlap=ov), o)
 
 
 @pytest.mark.parametrize("look", LOOKS)
-def test_klee_minty(sx, look):
+def test_klee_minty(sx, look, ov):
     A, b, c = F.klee_minty(9)                      # 511 pivots, many repeated pivot rows
     o = oracle.solve(A, b, c, max_pivots=600, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, max_pivots=600, lookahead=look), o)
+    assert_same(gpu_solve(sx, A, b, c, max_pivots=600, lookahead=look, overlap=ov), o)
 
 
 @pytest.mark.parametrize("look", LOOKS)
 @pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
-def test_dense_64(sx, seed, look):
+def test_dense_64(sx, seed, look, ov):
     A, b, c = lpgen.dense_lp(64, 64, seed)
     o = oracle.solve(A, b, c, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, lookahead=look), o)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=look, overlap=ov), o)
 
 
 @pytest.mark.parametrize("look", [3, 8, 16])
 @pytest.mark.parametrize("seed", range(10))
-def test_tie_heavy(sx, seed, look):
+def test_tie_heavy(sx, seed, look, ov):
     rng = np.random.default_rng(seed)
     m, n = int(rng.integers(3, 40)), int(rng.integers(3, 40))
     A, b, c = F.tie_heavy(m, n, seed)
     A[:, A.sum(axis=0) == 0] = 1.0
     o = oracle.solve(A, b, c, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, lookahead=look), o)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=look, overlap=ov), o)
 
 
 @pytest.mark.parametrize("look", [5, 16])
 @pytest.mark.parametrize("m,n", [(1, 1), (1, 700), (700, 1), (3, 1500), (257, 513), (1100, 90)])
-def test_ragged_shapes(sx, m, n, look):
+def test_ragged_shapes(sx, m, n, look, ov):
     A, b, c = lpgen.dense_lp(m, n, 1000 + m + n)
     o = oracle.solve(A, b, c, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, lookahead=look), o)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=look, overlap=ov), o)
 
 
-def test_iteration_cap_inside_a_block(sx):
+def test_iteration_cap_inside_a_block(sx, ov):
     A, b, c = F.klee_minty(6)                      # 63 pivots; cap 21 falls inside a block of 8
     o = oracle.solve(A, b, c, max_pivots=21, keep_tableau=True)
     assert o.status == oracle.ITERATION_LIMIT
-    assert_same(gpu_solve(sx, A, b, c, max_pivots=21, lookahead=8), o)
+    assert_same(gpu_solve(sx, A, b, c, max_pivots=21, lookahead=8, overlap=ov), o)
 
 
-def test_iterate_stepwise_bitwise(sx):
+@pytest.mark.parametrize("seg", [8, 16, 40])
+def test_iterate_stepwise_bitwise(sx, ov, seg):
     A, b, c = lpgen.dense_lp(64, 64, 3)
-    with sx.Simplex(A, b, c, lookahead=8, segment_pivots=16) as s:
+    with sx.Simplex(A, b, c, lookahead=8, segment_pivots=seg, overlap=ov) as s:
         done_total = 0
         for step in (1, 3, 7, 8, 2, 16):
             done, st = s.iterate(step)
@@ -99,10 +107,10 @@ def test_iterate_stepwise_bitwise(sx):
 
 @pytest.mark.parametrize("key", [(1000, 1000, 1), (4000, 4000, 1)])
 @pytest.mark.parametrize("look", [8, 16])
-def test_golden(sx, key, look):
+def test_golden(sx, key, look, ov):
     g = np.load(os.path.join(GOLDEN_DIR, "dense_%dx%d_s%d.npz" % key))
     A, b, c = lpgen.dense_lp(*key)
-    with sx.Simplex(A, b, c, lookahead=look) as s:
+    with sx.Simplex(A, b, c, lookahead=look, overlap=ov) as s:
         st = s.solve()
         x, y, obj, piv, _ = s.solution()
         k, r = s.trace()
