@@ -113,6 +113,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 policy "evict first" for the streamed tableau (the look-ahead's working set stays in L2)
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_hint(double* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -794,6 +810,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
 
   const int c = blockIdx.x % nc;
   const int g = blockIdx.x / nc;
+  const uint64_t pol = l2_evict_first();
   const long long j0 = (long long)c * cw;
   const int jn = (int)min((long long)cw, ld - j0);                    // doubles in this chunk
   const int nr = rows > g ? (rows - g + Gr - 1) / Gr : 0;             // rows of this CTA
@@ -808,7 +825,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
         mbar_arrive_expect_tx(&full[k], (uint32_t)(rin * (jn + kMaxLook) * sizeof(double)));
         for (int rr = 0; rr < rin; ++rr) {
           const long long i = g + (long long)(n * R + rr) * Gr;
-          bulk_g2s(sT + ((size_t)k * R + rr) * cw, src + i * ld + j0, (uint32_t)(jn * sizeof(double)), &full[k]);
+          bulk_g2s_hint(sT + ((size_t)k * R + rr) * cw, src + i * ld + j0, (uint32_t)(jn * sizeof(double)), &full[k], pol);
           bulk_g2s(sC + ((size_t)k * R + rr) * kMaxLook, s.colS + i * kColS + bank * kMaxLook,
                    (uint32_t)(kMaxLook * sizeof(double)), &full[k]);
         }
@@ -864,7 +881,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         const int i = g + (n * R + rr) * Gr;
-        if (!((mark[i >> 5] >> (i & 31)) & 1u)) *reinterpret_cast<double2*>(dst + (long long)i * ld + j) = v[rr];
+        if (!((mark[i >> 5] >> (i & 31)) & 1u)) st_hint(dst + (long long)i * ld + j, v[rr], pol);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[k]);
@@ -884,7 +901,7 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
             v.y = __fma_rn(a, pr[u].y, v.y);
           }
         }
-        if (!((mark[i >> 5] >> (i & 31)) & 1u)) *reinterpret_cast<double2*>(dst + (long long)i * ld + j) = v;
+        if (!((mark[i >> 5] >> (i & 31)) & 1u)) st_hint(dst + (long long)i * ld + j, v, pol);
       }
     }
     __syncwarp();

@@ -1,6 +1,6 @@
 """Per-source-line stall samples / instructions from an ncu report (needs -lineinfo).
 
-    python scripts/ncu_hotspots.py report.ncu-rep [top]
+    python scripts/ncu_hotspots.py report.ncu-rep [top] [kernel-regex]
 """
 import csv
 import io
@@ -10,7 +10,8 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kfilt = ["--kernel-name", "regex:" + sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
 hdr_i = next(i for i, l in enumerate(lines) if l.startswith('"Line No"'))
