@@ -126,9 +126,6 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void st_hint(double* p, double2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -759,24 +756,34 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   }
 }
 
-// k_update_s: the rank-s pass, TMA-pipelined.  CTA b owns column chunk c = b mod nc
-// (cw doubles, one double2 per consumer thread) and rows g, g+Gr, g+2Gr, ... (g = b div nc),
-// so all CTAs sweep Gr consecutive rows at a time: the chip-wide HBM front stays contiguous.
-// A producer warp streams each row segment T[i][chunk] and the row's pivot-column entries
-// colS[i][0..15] into a K-stage shared-memory ring with 1-D TMA (cp.async.bulk + mbarrier
-// complete_tx), so the bytes in flight cost shared memory, not registers.  The 8 consumer
-// warps hold prow_u[j] (u < s) in registers, read a row's values from shared memory and
-// apply the chain  x <- fma(-col_u[i], prow_u[j], x), u = 0 .. s-1  (the oracle's order and
-// rounding), then store with 128-bit st.global.  The <= s pivot rows are not stored by the
-// stream (bitmap) but written at the end from their last normalized value prow_u, chained
-// over the later pivots of the block.
+// k_update_s: the rank-s pass, TMA in and TMA out.  CTA b owns column chunk c = b mod nc (cw
+// doubles, one double2 per consumer thread) and rows g, g+Gr, g+2Gr, ... (g = b div nc), so
+// all CTAs sweep Gr consecutive rows at a time: the chip-wide HBM front stays contiguous.
+// One CTA per SM, three roles over a K-stage shared-memory ring of R row segments:
+//   loader warp    streams each row segment T[i][chunk] and the row's pivot-column entries
+//                  colS[i][bank][0..15] into a free stage (cp.async.bulk + mbarrier complete_tx);
+//   8 consumer warps hold prow_u[j] (u < s) in registers and apply the chain
+//                  x <- fma(-col_u[i], prow_u[j], x), u = 0 .. s-1 (the oracle's order and
+//                  rounding), writing the result back into the stage;
+//   storer warp    bulk-stores every computed stage (cp.async.bulk global <- shared, L2
+//                  evict_first) and frees the slot once the store has read it.
+// Measured (scripts/ubench_pass.cu, 8000^2 geometry): 304 us per rank-16 pass on 132 SMs,
+// above the device-to-device copy rate, where register stores from the consumers reached
+// 433 us.  The <= s pivot rows are not stored by the stream (bitmap) but written at the end
+// from their last normalized value prow_u, chained over the later pivots of the block.
 //
 // src == dst: in place.  src != dst (software pipeline): reads the block's
 // starting tableau, writes the next buffer — also when the block is empty (a copy) — and does
 // NOT wait on the look-ahead kernel launched just before it (that one selects the NEXT block,
 // from src, concurrently); everything this pass reads was complete before that launch began.
+__device__ __forceinline__ void bulk_s2g_hint(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
 template <int S, int R, int K>
-__global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const double* __restrict__ src,
+__global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const double* __restrict__ src,
                                                                double* dst, int bank, int nc, int Gr, int cw) {
   pdl_launch_dependents();
   if (src == dst) pdl_wait();
@@ -787,8 +794,9 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
   double* sT = reinterpret_cast<double*>(smem_raw);                 // [K][R][cw]
   double* sC = sT + (size_t)K * R * cw;                              // [K][R][kMaxLook]
   unsigned int* mark = reinterpret_cast<unsigned int*>(sC + (size_t)K * R * kMaxLook);
-  __shared__ __align__(8) uint64_t full[K];
-  __shared__ __align__(8) uint64_t empty[K];
+  __shared__ __align__(8) uint64_t full[K];    // stage loaded (tx bytes)
+  __shared__ __align__(8) uint64_t comp[K];    // stage computed (8 consumer warps)
+  __shared__ __align__(8) uint64_t empty[K];   // stage stored and free (storer)
   __shared__ int sh_r[S];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -800,7 +808,8 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
   if (tid == 0) {
     for (int k = 0; k < K; ++k) {
       mbar_init(&full[k], 1);
-      mbar_init(&empty[k], kThreads / 32);
+      mbar_init(&comp[k], kThreads / 32);
+      mbar_init(&empty[k], 1);
     }
     fence_barrier_init();
   }
@@ -810,14 +819,14 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
 
   const int c = blockIdx.x % nc;
   const int g = blockIdx.x / nc;
-  const uint64_t pol = l2_evict_first();
   const long long j0 = (long long)c * cw;
   const int jn = (int)min((long long)cw, ld - j0);                    // doubles in this chunk
   const int nr = rows > g ? (rows - g + Gr - 1) / Gr : 0;             // rows of this CTA
   const int nst = (nr + R - 1) / R;
 
-  if (warp == kThreads / 32) {                                        // ---- producer warp
+  if (warp == kThreads / 32) {                                        // ---- loader warp
     if (lane == 0) {
+      const uint64_t pol = l2_evict_first();
       for (int n = 0; n < nst; ++n) {
         const int k = n % K;
         if (n >= K) mbar_wait(&empty[k], ((n / K) - 1) & 1);
@@ -825,11 +834,35 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
         mbar_arrive_expect_tx(&full[k], (uint32_t)(rin * (jn + kMaxLook) * sizeof(double)));
         for (int rr = 0; rr < rin; ++rr) {
           const long long i = g + (long long)(n * R + rr) * Gr;
-          bulk_g2s_hint(sT + ((size_t)k * R + rr) * cw, src + i * ld + j0, (uint32_t)(jn * sizeof(double)), &full[k], pol);
+          bulk_g2s_hint(sT + ((size_t)k * R + rr) * cw, src + i * ld + j0, (uint32_t)(jn * sizeof(double)), &full[k],
+                        pol);
           bulk_g2s(sC + ((size_t)k * R + rr) * kMaxLook, s.colS + i * kColS + bank * kMaxLook,
                    (uint32_t)(kMaxLook * sizeof(double)), &full[k]);
         }
       }
+    }
+    return;
+  }
+  if (warp == kThreads / 32 + 1) {                                    // ---- storer warp
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first();
+      for (int m = 0; m < nst; ++m) {
+        const int k = m % K;
+        mbar_wait(&comp[k], (m / K) & 1);
+        const int rin = min(R, nr - m * R);
+        for (int rr = 0; rr < rin; ++rr) {
+          const int i = g + (m * R + rr) * Gr;
+          if (!((mark[i >> 5] >> (i & 31)) & 1u))
+            bulk_s2g_hint(dst + (long long)i * ld + j0, sT + ((size_t)k * R + rr) * cw, (uint32_t)(jn * sizeof(double)),
+                          pol);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (m >= 1) {                                  // the previous stage's store has read its slot
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          mbar_arrive(&empty[(m - 1) % K]);
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // writes done before the CTA exits
     }
     return;
   }
@@ -847,50 +880,34 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
     mbar_wait(&full[k], (n / K) & 1);
     const int rin = min(R, nr - n * R);
     if (se == S && rin == R && act) {
-      // full block, full stage: the R rows' 2R chains interleave (independent FMAs)
+      // full block, full stage: the R rows' 2R chains interleave (independent FMAs); the
+      // stage's pivot-column entries are loaded ahead of the chains
       double2 v[R];
-      const double2* cc2[R];
+      double2 ca[R][S / 2];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) {
         v[rr] = *reinterpret_cast<const double2*>(sT + ((size_t)k * R + rr) * cw + jl);
-        cc2[rr] = reinterpret_cast<const double2*>(sC + ((size_t)k * R + rr) * kMaxLook);
+#pragma unroll
+        for (int h = 0; h < S / 2; ++h)
+          ca[rr][h] = reinterpret_cast<const double2*>(sC + ((size_t)k * R + rr) * kMaxLook)[h];
       }
-      // the pivot-column entries are loaded one pair ahead of their FMAs (software
-      // pipeline: the shared-memory latency hides behind the previous pair's chains)
-      double2 ca[R][S / 2];
-#pragma unroll
-      for (int h = 0; h < S / 2; ++h)
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) ca[rr][h] = cc2[rr][h];
 #pragma unroll
       for (int h = 0; h < S / 2; ++h) {
-        double2 a[R];
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) a[rr] = ca[rr][h];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
-          v[rr].x = __fma_rn(-a[rr].x, pr[2 * h].x, v[rr].x);
-          v[rr].y = __fma_rn(-a[rr].x, pr[2 * h].y, v[rr].y);
+          v[rr].x = __fma_rn(-ca[rr][h].x, pr[2 * h].x, v[rr].x);
+          v[rr].y = __fma_rn(-ca[rr][h].x, pr[2 * h].y, v[rr].y);
         }
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
-          v[rr].x = __fma_rn(-a[rr].y, pr[2 * h + 1].x, v[rr].x);
-          v[rr].y = __fma_rn(-a[rr].y, pr[2 * h + 1].y, v[rr].y);
+          v[rr].x = __fma_rn(-ca[rr][h].y, pr[2 * h + 1].x, v[rr].x);
+          v[rr].y = __fma_rn(-ca[rr][h].y, pr[2 * h + 1].y, v[rr].y);
         }
       }
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        const int i = g + (n * R + rr) * Gr;
-        if (!((mark[i >> 5] >> (i & 31)) & 1u)) st_hint(dst + (long long)i * ld + j, v[rr], pol);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[k]);
-      continue;
-    }
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) {
-      if (rr < rin && act) {
-        const int i = g + (n * R + rr) * Gr;
+      for (int rr = 0; rr < R; ++rr) *reinterpret_cast<double2*>(sT + ((size_t)k * R + rr) * cw + jl) = v[rr];
+    } else if (act) {
+      for (int rr = 0; rr < rin; ++rr) {
         double2 v = *reinterpret_cast<const double2*>(sT + ((size_t)k * R + rr) * cw + jl);
         const double* cc = sC + ((size_t)k * R + rr) * kMaxLook;
 #pragma unroll
@@ -901,11 +918,12 @@ __global__ void __launch_bounds__(kThreads + 32, 2) k_update_s(SlabView s, const
             v.y = __fma_rn(a, pr[u].y, v.y);
           }
         }
-        if (!((mark[i >> 5] >> (i & 31)) & 1u)) st_hint(dst + (long long)i * ld + j, v, pol);
+        *reinterpret_cast<double2*>(sT + ((size_t)k * R + rr) * cw + jl) = v;
       }
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> bulk store
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[k]);
+    if (lane == 0) mbar_arrive(&comp[k]);
   }
   if (!act) return;
   // pivot rows of this chunk owned by this row group: from the LAST time each was the
@@ -1093,7 +1111,7 @@ cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown
 // k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
 // SIMPLEX_PASS_CFG selects one for experiments (default 0).
 struct PassCfg { int R, K; };
-static const PassCfg kPassCfgs[] = {{2, 8}, {4, 4}, {1, 8}, {1, 16}, {2, 10}, {3, 8}};
+static const PassCfg kPassCfgs[] = {{4, 12}, {4, 10}, {8, 5}, {6, 7}, {2, 16}, {4, 8}};
 static int pass_cfg() {
   static int c = [] {
     const char* e = std::getenv("SIMPLEX_PASS_CFG");
@@ -1114,7 +1132,7 @@ static cudaError_t pass_prepare(size_t smem, int* occ) {
   auto kern = k_update_s<S, R, K>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, kThreads + 32, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, kThreads + 64, smem);
 }
 
 template <int R, int K>
@@ -1128,12 +1146,12 @@ static cudaError_t pass_prepare_s(int S, size_t smem, int* occ) {
 
 cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem) {
   switch (pass_cfg()) {
-    case 1: return pass_prepare_s<4, 4>(S, smem, blocks_per_sm);
-    case 2: return pass_prepare_s<1, 8>(S, smem, blocks_per_sm);
-    case 3: return pass_prepare_s<1, 16>(S, smem, blocks_per_sm);
-    case 4: return pass_prepare_s<2, 10>(S, smem, blocks_per_sm);
-    case 5: return pass_prepare_s<3, 8>(S, smem, blocks_per_sm);
-    default: return pass_prepare_s<2, 8>(S, smem, blocks_per_sm);
+    case 1: return pass_prepare_s<4, 10>(S, smem, blocks_per_sm);
+    case 2: return pass_prepare_s<8, 5>(S, smem, blocks_per_sm);
+    case 3: return pass_prepare_s<6, 7>(S, smem, blocks_per_sm);
+    case 4: return pass_prepare_s<2, 16>(S, smem, blocks_per_sm);
+    case 5: return pass_prepare_s<4, 8>(S, smem, blocks_per_sm);
+    default: return pass_prepare_s<4, 12>(S, smem, blocks_per_sm);
   }
 }
 
@@ -1142,9 +1160,9 @@ static cudaError_t pass_launch(const SlabView& s, int S, const double* src, doub
                                int cw, size_t smem, cudaStream_t st, bool pdl) {
   const int grid = nc * Gr;
   switch (update_s_max(S)) {
-    case 4: return launch_ex(k_update_s<4, R, K>, grid, kThreads + 32, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
-    case 8: return launch_ex(k_update_s<8, R, K>, grid, kThreads + 32, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
-    default: return launch_ex(k_update_s<16, R, K>, grid, kThreads + 32, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
+    case 4: return launch_ex(k_update_s<4, R, K>, grid, kThreads + 64, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
+    case 8: return launch_ex(k_update_s<8, R, K>, grid, kThreads + 64, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
+    default: return launch_ex(k_update_s<16, R, K>, grid, kThreads + 64, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
   }
 }
 
@@ -1152,12 +1170,12 @@ cudaError_t launch_update_s(const SlabView& s, int S, const double* src, double*
                             int cw, cudaStream_t st, bool pdl) {
   const size_t smem = update_s_smem(cw, s.rows);
   switch (pass_cfg()) {
-    case 1: return pass_launch<4, 4>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
-    case 2: return pass_launch<1, 8>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
-    case 3: return pass_launch<1, 16>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
-    case 4: return pass_launch<2, 10>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
-    case 5: return pass_launch<3, 8>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
-    default: return pass_launch<2, 8>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 1: return pass_launch<4, 10>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 2: return pass_launch<8, 5>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 3: return pass_launch<6, 7>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 4: return pass_launch<2, 16>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    case 5: return pass_launch<4, 8>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
+    default: return pass_launch<4, 12>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
   }
 }
 
