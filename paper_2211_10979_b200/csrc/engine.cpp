@@ -113,6 +113,8 @@ struct simplex_s {
   int S = 32;                       // pivots per captured graph segment
   int look = 1;                     // pivots per tableau pass (>1: rank-s look-ahead)
   bool overlap = false;             // look-ahead software pipeline: select block b+1 during pass b
+  bool look_cache = true;           // pipelined selection keeps the previous bank in shared memory
+  int pass_cfg = 0;                 // k_update_s configuration (kernels.cu kPassCfgs)
   bool pdl = true;                  // programmatic dependent launch between pivot kernels
   bool force_nccl = false;          // test hook: 1-rank NCCL exchange on one GPU
   bool graphs_ready = false;
@@ -211,6 +213,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   cap = opt.max_pivots > 0 ? opt.max_pivots : 20 * (m + n);
   S = opt.segment_pivots > 0 ? opt.segment_pivots : 32;
   if (const char* e = std::getenv("SIMPLEX_NO_PDL")) pdl = !(e[0] == '1');
+  if (const char* e = std::getenv("SIMPLEX_NO_LOOK_CACHE")) look_cache = !(e[0] == '1');   // experiment hook
   if (const char* e = std::getenv("SIMPLEX_FORCE_NCCL")) force_nccl = (e[0] == '1') && nranks == 1 && nslabs == 1;
   // 0 = automatic: rank-16 look-ahead on one column part, one pivot per pass otherwise
   look = opt.lookahead > 0 ? opt.lookahead : ((nparts == 1 && !force_nccl) ? sx::kMaxLook : 1);
@@ -273,7 +276,8 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       // 296 CTAs at 8000^2 instead of 32 x 9 = 288)
       const int cwmax = 2 * sx::kThreads;
       int occ = 1;
-      CK(sx::update_s_occupancy(look, &occ, sx::update_s_smem(cwmax, v.rows)));
+      pass_cfg = sx::pass_cfg_choice(overlap);
+      CK(sx::update_s_occupancy(pass_cfg, look, &occ, sx::update_s_smem(pass_cfg, cwmax, v.rows)));
       if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
       const char* ps = getenv("SIMPLEX_PASS_SMS");          // experiment hook
       const long long slots = (long long)occ * (ps ? atoi(ps) : overlap ? sms - sl.look_grid : sms);
@@ -414,22 +418,22 @@ simplex_err simplex_s::enqueue_pivot(int slot, int t) {
       double* buf[2] = {sl.v.T, sl.T2};
       static const bool time_sel = std::getenv("SIMPLEX_TIME_SELECT") != nullptr;   // experiment hook
       if (opt.time_kernels && time_sel) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
-      CK(sx::launch_lookahead(sl.v, buf[q], look, q ^ 1, q, opt.tol_opt, opt.tol_piv, sl.look_grid, stream));
+      CK(sx::launch_lookahead(sl.v, buf[q], look, q ^ 1, q, opt.tol_opt, opt.tol_piv, sl.look_grid, look_cache, stream));
       if (opt.time_kernels)
         CK(cudaEventRecordWithFlags(tev[slot][2 * t + (time_sel ? 1 : 0)], stream, cudaEventRecordExternal));
       if (opt.time_kernels && time_sel) {
-        CK(sx::launch_update_s(sl.v, look, buf[q], buf[q ^ 1], q, sl.nc, sl.Gr, sl.cw, stream, false));
+        CK(sx::launch_update_s(pass_cfg, sl.v, look, buf[q], buf[q ^ 1], q, sl.nc, sl.Gr, sl.cw, stream, false));
         return SIMPLEX_OK;
       }
-      CK(sx::launch_update_s(sl.v, look, buf[q], buf[q ^ 1], q, sl.nc, sl.Gr, sl.cw, stream,
+      CK(sx::launch_update_s(pass_cfg, sl.v, look, buf[q], buf[q ^ 1], q, sl.nc, sl.Gr, sl.cw, stream,
                              pdl && !opt.time_kernels));
       if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
       return SIMPLEX_OK;
     }
     // rank-s block: select up to `look` pivots ahead, then one pass applies them all in place
-    CK(sx::launch_lookahead(sl.v, sl.v.T, look, 0, -1, opt.tol_opt, opt.tol_piv, sl.look_grid, stream));
+    CK(sx::launch_lookahead(sl.v, sl.v.T, look, 0, -1, opt.tol_opt, opt.tol_piv, sl.look_grid, false, stream));
     if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
-    CK(sx::launch_update_s(sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, pdl && !opt.time_kernels));
+    CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, pdl && !opt.time_kernels));
     if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
     return SIMPLEX_OK;
   }
@@ -506,7 +510,7 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
     if (overlap) {
       // pipeline prologue: the first block is selected from the current tableau into bank 0
       const Slab& sl = slabs[0];
-      CK(sx::launch_lookahead(sl.v, sl.v.T, look, 0, -1, opt.tol_opt, opt.tol_piv, sl.look_grid, stream));
+      CK(sx::launch_lookahead(sl.v, sl.v.T, look, 0, -1, opt.tol_opt, opt.tol_piv, sl.look_grid, false, stream));
       ++kernel_launches;
     }
     long long launched = 0, completed = 0, seen = it;
@@ -543,7 +547,7 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
     if (overlap) {
       // pipeline drain: the last selected block (bank 0) is applied in place to buffer 0
       const Slab& sl = slabs[0];
-      CK(sx::launch_update_s(sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
+      CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
       ++kernel_launches;
     }
     // Phase I optimal: decide feasibility, drive artificials out, install the objective

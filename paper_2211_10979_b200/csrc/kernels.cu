@@ -517,7 +517,8 @@ __device__ __forceinline__ void cluster_barrier() {
 // EVERY CTA's shared memory (DSMEM st.shared::cluster), one cluster barrier, and every
 // CTA folds its local copy.  `slot` is double-buffered by `ph` (a CTA can be at most one
 // reduction ahead of another), so two consecutive reductions never share a slot.
-__device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph) {
+__device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const double* pf_rows = nullptr,
+                                            long long pf_ld = 0) {
   __shared__ Cand sh_w[32];
   __shared__ Cand sh_res;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -538,6 +539,12 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph) {
                    "l"(t.idx)
                    : "memory");
     }
+    // row candidates: start pulling this CTA's best row into L2 while the cluster agrees on
+    // the winner (one of the nct CTA bests), so the next phase reads it from L2, not HBM
+    if (pf_rows && lane == 0 && t.idx != LLONG_MAX)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf_rows + (long long)cand_row(t.idx) * pf_ld),
+                   "r"((uint32_t)(pf_ld * sizeof(double)))
+                   : "memory");
   }
   cluster_barrier();
   if (wid == 0) {
@@ -584,7 +591,8 @@ cudaError_t lprof_read(unsigned long long* out) {
 // loads a phase needs (per-step scalars, the T entry, the pending chain operands) are issued
 // before the first dependent use, so each phase costs about one memory latency.
 __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const double* __restrict__ T, int S,
-                                                           int bown, int bpre, double tol_opt, double tol_piv) {
+                                                           int bown, int bpre, int nqc, int nqr, double tol_opt,
+                                                           double tol_piv) {
   pdl_launch_dependents();                            // the previous block's pass may start now
   DevState* st = s.st;
   __shared__ int sh_r[kMaxLook];                      // own pivot rows
@@ -609,6 +617,27 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   const long long cap = st->cap;
   const int spre = bpre >= 0 ? st->sb[bpre] : 0;
   int ph = 0;
+  // nqc > 0: the previous bank's operands of this thread's columns / rows are read ONCE into
+  // shared memory (the same values are chained at every step of this launch):
+  //   cP[(u * nqc + q) * blockDim + tid] = prow_u[j_q],  cR[(u * nqr + q) * blockDim + tid] = col_u[i_q]
+  const int mwords = ((rows + 31) / 32 + 3) & ~3;
+  double* cP = reinterpret_cast<double*>(piv_mark + mwords);
+  double* cR = cP + (size_t)kMaxLook * nqc * blockDim.x;
+  const bool cache = nqc > 0 && spre > 0;
+  if (cache) {
+    for (int q = 0; q < nqc; ++q) {
+      const long long j = gtid + (long long)q * gthreads;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u)
+        if (u < spre) cP[((size_t)u * nqc + q) * blockDim.x + threadIdx.x] = j < ld ? prowP[(long long)u * ld + j] : 0.0;
+    }
+    for (int q = 0; q < nqr; ++q) {
+      const long long i = gtid + (long long)q * gthreads;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u)
+        if (u < spre) cR[((size_t)u * nqr + q) * blockDim.x + threadIdx.x] = i < rows ? colP[i * kColS + u] : 0.0;
+    }
+  }
   for (int q = threadIdx.x; q < (rows + 31) / 32; q += blockDim.x) piv_mark[q] = 0u;
   if (threadIdx.x < kMaxLook) sh_rp[threadIdx.x] = (int)threadIdx.x < spre ? st->rsb[bpre][threadIdx.x] : -1;
   __syncthreads();
@@ -649,12 +678,14 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     for (int u = 0; u < kMaxLook; ++u) pk[u] = u < t ? __ldcg(prowO + (long long)u * ld + k) : 0.0;
     const double pw_prev = r_prev >= 0 ? __ldcg(p_prev + w) : 0.0;
     Cand rb = cand_none();
-    for (long long i = gtid; i < rows; i += gthreads) {
+    int qi = 0;
+    for (long long i = gtid; i < rows; i += gthreads, ++qi) {
       double x = T[i * ld + k];
       double h = RHS[i];
       double cq[kMaxLook], cu[kMaxLook];                // this row's pending-column entries
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) cq[u] = u < spre ? colP[i * kColS + u] : 0.0;
+      for (int u = 0; u < kMaxLook; ++u)
+        cq[u] = u < spre ? (cache ? cR[((size_t)u * nqr + qi) * blockDim.x + threadIdx.x] : colP[i * kColS + u]) : 0.0;
 #pragma unroll
       for (int u = 0; u < kMaxLook; ++u) cu[u] = u < t ? colO[i * kColS + u] : 0.0;
       if (r_prev >= 0) h = (i == r_prev) ? pw_prev : __fma_rn(-c_prev[i * kColS], pw_prev, h);
@@ -679,7 +710,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
         rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
     }
     SX_LPROF(4 * t + 1);
-    rb = cluster_min(rb, slot, ph);
+    rb = cluster_min(rb, slot, ph, T, ld);
     SX_LPROF(4 * t + 2);
     ph ^= 1;
     if (rb.idx == LLONG_MAX) {                                                 // unbounded
@@ -706,12 +737,15 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
       if (u < spre && sh_rp[u] == r) qmask |= 1u << u;
     }
     best = cand_none();
-    for (long long j = gtid; j < ld; j += gthreads) {
+    int qj = 0;
+    for (long long j = gtid; j < ld; j += gthreads, ++qj) {
       double x = Tr[j];
       const double r0 = R0[j];
       double qu[kMaxLook], pu[kMaxLook];                // this column's pending-row entries
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) qu[u] = u < spre ? prowP[(long long)u * ld + j] : 0.0;
+      for (int u = 0; u < kMaxLook; ++u)
+        qu[u] = u < spre ? (cache ? cP[((size_t)u * nqc + qj) * blockDim.x + threadIdx.x] : prowP[(long long)u * ld + j])
+                         : 0.0;
 #pragma unroll
       for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? prowO[(long long)u * ld + j] : 0.0;
 #pragma unroll
@@ -1088,6 +1122,7 @@ static cudaLaunchConfig_t lookahead_config(int cluster, size_t smem, cudaStream_
 // Largest cluster (16, else 8, 4, 2, 1 CTAs) the device can co-schedule for k_lookahead.
 int lookahead_cluster_size() {
   cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLookCacheMax);
   const char* e = std::getenv("SIMPLEX_LOOK_CLUSTER");   // experiment hook: cap the cluster size
   const int cmax = e ? std::atoi(e) : 16;
   for (int c : {16, 8, 4, 2, 1}) {
@@ -1101,29 +1136,44 @@ int lookahead_cluster_size() {
   return 0;
 }
 
+// Shared memory of k_lookahead: the pivot-row bitmap, plus (nqc > 0) the previous bank's chain
+// operands of every thread's columns and rows.  0 if that cache does not fit.
+size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int* nqr) {
+  const long long gthreads = (long long)cluster * kLookThreads;
+  const size_t mark = (size_t)(((s.rows + 31) / 32 + 3) & ~3) * sizeof(unsigned int);
+  *nqc = (int)((s.ld + gthreads - 1) / gthreads);
+  *nqr = (int)((s.rows + gthreads - 1) / gthreads);
+  const size_t c = (size_t)kMaxLook * sizeof(double) * kLookThreads * (*nqc + *nqr);
+  if (cache && mark + c <= kLookCacheMax) return mark + c;
+  *nqc = *nqr = 0;
+  return mark;
+}
+
 cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
-                             double tol_piv, int cluster, cudaStream_t st) {
+                             double tol_piv, int cluster, bool cache, cudaStream_t st) {
+  int nqc = 0, nqr = 0;
+  const size_t smem = lookahead_smem(s, cluster, cache && bpre >= 0, &nqc, &nqr);
   cudaLaunchAttribute attr[1];
-  cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((s.rows + 31) / 32) * sizeof(unsigned int), st, attr);
-  return cudaLaunchKernelEx(&cfg, k_lookahead, s, T, S, bown, bpre, tol_opt, tol_piv);
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, smem, st, attr);
+  return cudaLaunchKernelEx(&cfg, k_lookahead, s, T, S, bown, bpre, nqc, nqr, tol_opt, tol_piv);
 }
 
 // k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
-// SIMPLEX_PASS_CFG selects one for experiments (default 0).
+// Measured at 8000^2 (scripts/pipe_sweep.sh): {4, 12} is the fastest pass on its own; next to
+// the concurrent look-ahead selection the gentler {2, 16} gives the shorter pipelined block.
+// SIMPLEX_PASS_CFG overrides the choice (experiments).
 struct PassCfg { int R, K; };
 static const PassCfg kPassCfgs[] = {{4, 12}, {4, 10}, {8, 5}, {6, 7}, {2, 16}, {4, 8}};
-static int pass_cfg() {
-  static int c = [] {
-    const char* e = std::getenv("SIMPLEX_PASS_CFG");
-    const int v = e ? std::atoi(e) : 0;
-    return (v >= 0 && v < 6) ? v : 0;
-  }();
-  return c;
+int pass_cfg_choice(bool pipelined) {
+  const char* e = std::getenv("SIMPLEX_PASS_CFG");
+  const int v = e ? std::atoi(e) : -1;
+  if (v >= 0 && v < 6) return v;
+  return pipelined ? 4 : 0;
 }
 int update_s_max(int S) { return S <= 4 ? 4 : S <= 8 ? 8 : 16; }
 
-size_t update_s_smem(int cw, int rows) {
-  const PassCfg c = kPassCfgs[pass_cfg()];
+size_t update_s_smem(int cfg, int cw, int rows) {
+  const PassCfg c = kPassCfgs[cfg];
   return (size_t)c.K * c.R * (cw + kMaxLook) * sizeof(double) + (size_t)((rows + 31) / 32) * sizeof(unsigned int);
 }
 
@@ -1144,8 +1194,8 @@ static cudaError_t pass_prepare_s(int S, size_t smem, int* occ) {
   }
 }
 
-cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem) {
-  switch (pass_cfg()) {
+cudaError_t update_s_occupancy(int cfg, int S, int* blocks_per_sm, size_t smem) {
+  switch (cfg) {
     case 1: return pass_prepare_s<4, 10>(S, smem, blocks_per_sm);
     case 2: return pass_prepare_s<8, 5>(S, smem, blocks_per_sm);
     case 3: return pass_prepare_s<6, 7>(S, smem, blocks_per_sm);
@@ -1166,10 +1216,10 @@ static cudaError_t pass_launch(const SlabView& s, int S, const double* src, doub
   }
 }
 
-cudaError_t launch_update_s(const SlabView& s, int S, const double* src, double* dst, int bank, int nc, int Gr,
-                            int cw, cudaStream_t st, bool pdl) {
-  const size_t smem = update_s_smem(cw, s.rows);
-  switch (pass_cfg()) {
+cudaError_t launch_update_s(int cfg, const SlabView& s, int S, const double* src, double* dst, int bank, int nc,
+                            int Gr, int cw, cudaStream_t st, bool pdl) {
+  const size_t smem = update_s_smem(cfg, cw, s.rows);
+  switch (cfg) {
     case 1: return pass_launch<4, 10>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
     case 2: return pass_launch<8, 5>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
     case 3: return pass_launch<6, 7>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);

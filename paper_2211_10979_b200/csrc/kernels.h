@@ -20,15 +20,19 @@ cudaError_t update_occupancy(int* blocks_per_sm);
 cudaError_t launch_update(const SlabView& s, int q, double tol_opt, int grid, cudaStream_t st, bool pdl);
 // k_lookahead: select up to S pivots into chain bank `bown`, chaining from T (bpre >= 0: first
 // the pending pivots of bank bpre, whose pass runs concurrently)
+// (cache: keep the previous bank's operands in shared memory when they fit)
+constexpr size_t kLookCacheMax = 200 * 1024;
 cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
-                             double tol_piv, int cluster, cudaStream_t st);
+                             double tol_piv, int cluster, bool cache, cudaStream_t st);
+size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int* nqr);
 int lookahead_cluster_size();
 int update_s_max(int S);
-size_t update_s_smem(int cw, int rows);
-cudaError_t update_s_occupancy(int S, int* blocks_per_sm, size_t smem);
+int pass_cfg_choice(bool pipelined);     // k_update_s configuration index (R rows x K stages)
+size_t update_s_smem(int cfg, int cw, int rows);
+cudaError_t update_s_occupancy(int cfg, int S, int* blocks_per_sm, size_t smem);
 // k_update_s: apply the pivots of chain bank `bank` to src, writing dst (src == dst: in place)
-cudaError_t launch_update_s(const SlabView& s, int S, const double* src, double* dst, int bank, int nc, int Gr,
-                            int cw, cudaStream_t st, bool pdl);
+cudaError_t launch_update_s(int cfg, const SlabView& s, int S, const double* src, double* dst, int bank, int nc,
+                            int Gr, int cw, cudaStream_t st, bool pdl);
 cudaError_t launch_phase1_row0(const SlabView& s, cudaStream_t st);
 cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st);
 cudaError_t launch_force(const SlabView& s, int r, int k, cudaStream_t st);
