@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--lookahead", type=int, default=0,
                     help="pivots per tableau pass (0: library default = 16 on one column part, 1 with "
                          "N > 1; 1: one pass per pivot; 2..16: rank-s look-ahead)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="rank-s look-ahead without the software pipeline (select, then pass)")
     ap.add_argument("--pivot-rule", default="dantzig", choices=["dantzig", "bland"],
                     help="entering/leaving rule (bland = SURVEY.md §8(f) NEXT #3)")
     ap.add_argument("--single-pass-pivots", type=int, default=1000,
@@ -92,13 +94,14 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def ncu_traffic(workload, nranks):
-    """dram read+write bytes per k_update launch from a committed ncu --set full capture."""
+def ncu_traffic(workload, nranks, look=1):
+    """dram read+write bytes per pass launch (k_update, or k_update_s for look > 1) from a
+    committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "ncu_update_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
-    e = d.get(f"{workload}/p{nranks}")
+    e = d.get(f"{workload}/s{look}/p{nranks}" if look > 1 else f"{workload}/p{nranks}")
     return e.get("dram_bytes_per_launch") if e else None
 
 
@@ -244,7 +247,8 @@ def main():
     torch.cuda.synchronize()
 
     rule = sx.BLAND if args.pivot_rule == "bland" else sx.DANTZIG
-    solver = sx.Simplex(dA, db, dc, group=group, lookahead=args.lookahead, pivot_rule=rule)
+    solver = sx.Simplex(dA, db, dc, group=group, lookahead=args.lookahead, pivot_rule=rule,
+                        overlap=not args.no_overlap)
     st = solver.stats()
     tableau_bytes = 8 * (m + 1) * (n + m + 1)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -315,7 +319,8 @@ def main():
     # (event-record nodes in the captured graph, on the stream the kernel runs on).  Kept
     # out of the value steps because an event node between two pivot kernels disables the
     # programmatic-dependent-launch edge the production loop uses.
-    prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule)
+    prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule,
+                      overlap=not args.no_overlap)
     barrier()
     window = min(piv, args.roofline_pivots)
     prof.iterate(window)
@@ -384,6 +389,9 @@ def main():
                                    + ("Dantzig + lowest-index ties" if args.pivot_rule == "dantzig" else
                                       "Bland's rule"), "m": m, "n": n, "pivots_per_solve": piv,
                        "pivots_per_tableau_pass": look,
+                       "schedule": ("select block b+1 (16-SM cluster) concurrently with the pass of block b "
+                                    "(two tableau buffers)" if look > 1 and not args.no_overlap else
+                                    "select, then pass" if look > 1 else "one pivot per pass"),
                        "time_to_solve_ms": total_ms / args.steps,
                        "parallelism": f"column slabs x{world}" + (" (NCCL allgather/pivot)" if world > 1 else ""),
                        "l2": ("tableau %.2f GB > L2 %d MB: inputs larger than L2" % (tableau_bytes / 1e9, l2 >> 20))
@@ -391,10 +399,11 @@ def main():
                        "step": "reset (build Table I from device-resident A,b,c) + solve + extract"},
             "roofline": {"bound": "hbm",
                          "kernel": (f"k_update_s (rank-{look} look-ahead pass: {look} pivots per tableau "
-                                    "stream, TMA-pipelined)") if look > 1 else
+                                    "stream, TMA loads + TMA bulk stores; runs concurrently with the "
+                                    "selection of the next block)") if look > 1 else
                                    "k_update (fused row-scale + rank-1 update)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "peak_source": peak_src, "traffic": ncu_traffic(args.workload, world),
+                         "peak_source": peak_src, "traffic": ncu_traffic(args.workload, world, look),
                          "bytes_per_launch": st.bytes_per_pivot,
                          "bytes_formula": "16*(m+1)*(local columns incl. rhs) per pivot",
                          "avg_launch_us": avg_upd_s * 1e6, "launches_timed": upd_launches,
