@@ -1,6 +1,8 @@
 """GPU parity of Bland's rule (pivot_rule = 1) against the oracle's
 or_solve_rule(rule=BLAND): identical traces and bit-identical tableaux on every path (one
 pivot per pass, rank-s look-ahead, column slabs)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -8,7 +10,7 @@ import lpgen
 import oracle
 from lpgen import fixtures as F
 
-from test_gpu_parity import assert_same, gpu_solve
+from test_gpu_parity import GOLDEN_DIR, assert_same, gpu_solve
 
 pytestmark = pytest.mark.gpu
 
@@ -73,3 +75,24 @@ def test_rule_validation(sx):
     with pytest.raises(sx.SimplexError) as e:
         sx.Simplex(A, b, c, pivot_rule=7)
     assert e.value.code == sx.E_ARG
+
+
+@pytest.mark.parametrize("overlap", [True, False], ids=["pipe", "serial"])
+def test_golden_4000_bland(sx, overlap):
+    """Bland's rule on the 4000x4000 benchmark LP runs into the 20(m+n) = 160000 cap: the whole
+    trace, the objective, x, y and the tableau digest against the oracle's 2-hour single-thread
+    run (tests/golden/dense_4000x4000_s1_bland.*, scripts/make_golden.py)."""
+    g = np.load(os.path.join(GOLDEN_DIR, "dense_4000x4000_s1_bland.npz"))
+    A, b, c = lpgen.dense_lp(4000, 4000, 1)
+    with sx.Simplex(A, b, c, pivot_rule=sx.BLAND, overlap=overlap) as s:
+        st = s.solve()
+        x, y, obj, piv, _ = s.solution()
+        k, r = s.trace()
+        h = s.tableau_hash()
+    assert st == int(g["status"]) == sx.ITERATION_LIMIT and piv == int(g["pivots"]) == 160000
+    assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+    assert obj == float(g["objective"]) and np.array_equal(y, g["y"])
+    xs = np.zeros(4000)
+    xs[g["x_idx"]] = g["x_val"]
+    assert np.array_equal(x, xs)
+    assert h == int(g["tableau_hash"])
