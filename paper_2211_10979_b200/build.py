@@ -16,10 +16,6 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsimplex.so")
-# profiling build (SIMPLEX_BUILD_PROFILE=1): %globaltimer stamps inside k_lookahead, separate .so
-PROFILE = os.environ.get("SIMPLEX_BUILD_PROFILE") == "1"
-if PROFILE:
-    LIB = os.path.join(PKG, "libsimplex_prof.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "engine.cpp")]
 DEPS = SOURCES + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
     [os.path.join(ROOT, "include", "libsimplex.h")]
@@ -67,7 +63,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
     ncclso = sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0]
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xptxas", "-v",
            "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared",
-           *(["-DSX_LOOK_PROFILE"] if PROFILE else []),
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            *SOURCES, "-o", LIB + ".tmp",
            "-L", lib, "-l:" + os.path.basename(ncclso), "-Xlinker", "-rpath," + lib]

@@ -855,11 +855,3 @@ simplex_err simplex_partition(int64_t total_cols, int64_t nparts, int64_t part, 
 const char* simplex_version(void) { return "libsimplex 0.1.0 (sm_100a, dense full-tableau simplex)"; }
 
 }  // extern "C"
-
-#ifdef SX_LOOK_PROFILE
-// Profiling builds only (SIMPLEX_BUILD_PROFILE=1): the last k_lookahead's phase time stamps.
-extern "C" simplex_err simplex_debug_lookahead_profile(uint64_t* out) {
-  CK(sx::lprof_read(reinterpret_cast<unsigned long long*>(out)));
-  return SIMPLEX_OK;
-}
-#endif

@@ -556,23 +556,6 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const do
   return sh_res;
 }
 
-#ifdef SX_LOOK_PROFILE
-// debug builds only: SM clock stamps (clock64: cheap, per-SM) of thread 0 per look-ahead step
-__device__ unsigned long long g_lprof[16 * (kMaxLook * 4 + 4)];
-#define SX_LPROF(slot)                                                   \
-  do {                                                                   \
-    if (threadIdx.x == 0 && blockIdx.x < 16) {                           \
-      unsigned long long t_;                                             \
-      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_) :: "memory");     \
-      g_lprof[blockIdx.x * (kMaxLook * 4 + 4) + (slot)] = t_;            \
-    }                                                                    \
-  } while (0)
-cudaError_t lprof_read(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, g_lprof, sizeof(g_lprof));
-}
-#else
-#define SX_LPROF(slot)
-#endif
 
 // k_lookahead: one thread-block cluster (one CTA per SM) selecting up to S pivots into chain
 // bank `bown`.  Per pivot t:
@@ -624,19 +607,32 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   double* cP = reinterpret_cast<double*>(piv_mark + mwords);
   double* cR = cP + (size_t)kMaxLook * nqc * blockDim.x;
   const bool cache = nqc > 0 && spre > 0;
-  if (cache) {
-    for (int q = 0; q < nqc; ++q) {
-      const long long j = gtid + (long long)q * gthreads;
+  if (cache) {                                        // async copies (LDGSTS): no register staging,
+    for (int q = 0; q < nqc; ++q) {                   // all in flight at once, overlapping the first
+      const long long j = gtid + (long long)q * gthreads;   // pricing scan and reduction
+      if (j < ld) {
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u)
-        if (u < spre) cP[((size_t)u * nqc + q) * blockDim.x + threadIdx.x] = j < ld ? prowP[(long long)u * ld + j] : 0.0;
+        for (int u = 0; u < kMaxLook; ++u)
+          if (u < spre)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             smem_u32(&cP[((size_t)u * nqc + q) * blockDim.x + threadIdx.x])),
+                         "l"(prowP + (long long)u * ld + j)
+                         : "memory");
+      }
     }
     for (int q = 0; q < nqr; ++q) {
       const long long i = gtid + (long long)q * gthreads;
+      if (i < rows) {
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u)
-        if (u < spre) cR[((size_t)u * nqr + q) * blockDim.x + threadIdx.x] = i < rows ? colP[i * kColS + u] : 0.0;
+        for (int u = 0; u < kMaxLook; ++u)
+          if (u < spre)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             smem_u32(&cR[((size_t)u * nqr + q) * blockDim.x + threadIdx.x])),
+                         "l"(colP + i * kColS + u)
+                         : "memory");
+      }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int q = threadIdx.x; q < (rows + 31) / 32; q += blockDim.x) piv_mark[q] = 0u;
   if (threadIdx.x < kMaxLook) sh_rp[threadIdx.x] = (int)threadIdx.x < spre ? st->rsb[bpre][threadIdx.x] : -1;
@@ -661,6 +657,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   best = cluster_min(best, slot, ph);                 // (its barriers also publish piv_mark)
   ph ^= 1;
 
+  if (cache) asm volatile("cp.async.wait_group 0;" ::: "memory");   // own entries only: no barrier
   int t = 0;
   int r_prev = spre > 0 ? sh_rp[spre - 1] : -1;       // pivot not yet applied to RHS
   const double* c_prev = spre > 0 ? colP + spre - 1 : nullptr;
@@ -669,7 +666,6 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     if (status != kRunning || it >= stop) break;
     if (best.idx == LLONG_MAX) { status = kOptimal; break; }                 // Step 1: optimal
     const long long k = best.idx;
-    SX_LPROF(4 * t);
     // ---- phase A: rows
     double qk[kMaxLook], pk[kMaxLook];                  // prow_u[k] of both banks (L2, same for all rows)
 #pragma unroll
@@ -709,9 +705,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
       if (i >= 1 && x > tol_piv)                                              // Step 2
         rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
     }
-    SX_LPROF(4 * t + 1);
     rb = cluster_min(rb, slot, ph, T, ld);
-    SX_LPROF(4 * t + 2);
     ph ^= 1;
     if (rb.idx == LLONG_MAX) {                                                 // unbounded
       status = kUnbounded;
@@ -776,11 +770,9 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     r_prev = r;
     c_prev = colO + t;
     p_prev = prow;
-    SX_LPROF(4 * t + 3);
     best = cluster_min(best, slot, ph);
     ph ^= 1;
   }
-  SX_LPROF(4 * kMaxLook);
   if (gtid == 0) {
     st->status = status;
     st->it = it;

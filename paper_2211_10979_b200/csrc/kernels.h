@@ -38,9 +38,6 @@ cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st);
 cudaError_t launch_force(const SlabView& s, int r, int k, cudaStream_t st);
 cudaError_t launch_set_status(DevState* d, int status, cudaStream_t st);
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st);
-#ifdef SX_LOOK_PROFILE
-cudaError_t lprof_read(unsigned long long* out);
-#endif
 cudaError_t launch_extract(const SlabView& s, long long n, double* x, double* y, double* obj, cudaStream_t st);
 cudaError_t launch_hash(const SlabView& s, long long Wg, int include_rhs, unsigned long long* out,
                         cudaStream_t st, int sms);
