@@ -276,7 +276,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       // 296 CTAs at 8000^2 instead of 32 x 9 = 288)
       const int cwmax = 2 * sx::kThreads;
       int occ = 1;
-      pass_cfg = sx::pass_cfg_choice(overlap);
+      pass_cfg = sx::pass_cfg_choice(overlap, 16.0 * v.rows * v.ld);   // bytes read + written per pass
       CK(sx::update_s_occupancy(pass_cfg, look, &occ, sx::update_s_smem(pass_cfg, cwmax, v.rows)));
       if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
       const char* ps = getenv("SIMPLEX_PASS_SMS");          // experiment hook

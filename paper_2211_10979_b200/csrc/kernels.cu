@@ -1151,16 +1151,18 @@ cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown
 }
 
 // k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
-// Measured at 8000^2 (scripts/pipe_sweep.sh): {4, 12} is the fastest pass on its own; next to
-// the concurrent look-ahead selection the gentler {2, 16} gives the shorter pipelined block.
+// Measured (scripts/pipe_sweep.sh): {4, 12} is the fastest pass on its own.  When the pass is
+// about as long as the concurrent look-ahead selection (tableaux up to a few GB: 2 GB at 8000^2)
+// the gentler {2, 16} gives the shorter pipelined block, because it slows the selection's
+// dependent HBM reads less; a larger tableau makes the pass the critical path again.
 // SIMPLEX_PASS_CFG overrides the choice (experiments).
 struct PassCfg { int R, K; };
 static const PassCfg kPassCfgs[] = {{4, 12}, {4, 10}, {8, 5}, {6, 7}, {2, 16}, {4, 8}};
-int pass_cfg_choice(bool pipelined) {
+int pass_cfg_choice(bool pipelined, double pass_bytes) {
   const char* e = std::getenv("SIMPLEX_PASS_CFG");
   const int v = e ? std::atoi(e) : -1;
   if (v >= 0 && v < 6) return v;
-  return pipelined ? 4 : 0;
+  return (pipelined && pass_bytes < 4e9) ? 4 : 0;
 }
 int update_s_max(int S) { return S <= 4 ? 4 : S <= 8 ? 8 : 16; }
 

@@ -27,7 +27,7 @@ cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown
 size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int* nqr);
 int lookahead_cluster_size();
 int update_s_max(int S);
-int pass_cfg_choice(bool pipelined);     // k_update_s configuration index (R rows x K stages)
+int pass_cfg_choice(bool pipelined, double pass_bytes);   // k_update_s configuration (R rows x K stages)
 size_t update_s_smem(int cfg, int cw, int rows);
 cudaError_t update_s_occupancy(int cfg, int S, int* blocks_per_sm, size_t smem);
 // k_update_s: apply the pivots of chain bank `bank` to src, writing dst (src == dst: in place)
