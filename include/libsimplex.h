@@ -105,8 +105,9 @@ typedef struct {
     int32_t  overlap;       /* rank-s look-ahead only.  1 (default): software pipeline —
                                block b+1 is selected (on one thread-block cluster) WHILE
                                block b's pass runs on the other SMs, out of place between
-                               two tableau buffers (2x the tableau's HBM); 0: select, then
-                               pass, in place.  Bitwise identical results either way.     */
+                               two tableau buffers (2x the tableau's HBM; falls back to 0
+                               when 2.2x the tableau exceeds the free device memory); 0:
+                               select, then pass, in place.  Bitwise identical results.    */
 } simplex_options;
 
 typedef struct {

@@ -241,6 +241,14 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   if (arts > 0 && (nparts > 1 || !opt.phase1))
     return fail(SIMPLEX_E_NEG_RHS, nparts > 1 ? "b has negative entries: Phase I runs on one column part only"
                                               : "b has a negative entry and phase1 = 0");
+  if (overlap) {
+    // the pipeline needs a second tableau buffer: fall back to select-then-pass in place when
+    // two tableaux (+10 %) do not fit in the free device memory
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const double tab = 8.0 * (double)(m + 1) * (double)roundup(W, 16);
+    if (2.2 * tab > (double)free_b) overlap = false;
+  }
 
   user_stream = static_cast<cudaStream_t>(opt.stream);
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
