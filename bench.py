@@ -351,6 +351,22 @@ def main():
                   "frac": st.bytes_per_pivot / a1 / 1e9 / peak, "launches_timed": s1p.update_launches,
                   "traffic": ncu_traffic(args.workload, world)}
 
+    # ---- the rank-s pass alone (select-then-pass schedule: all SMs, in place), for reference
+    alone = None
+    if look > 1 and not args.no_overlap and args.single_pass_pivots > 0:
+        p2 = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule,
+                        overlap=False)
+        barrier()
+        p2.iterate(min(piv, args.roofline_pivots))
+        barrier()
+        s2p = p2.stats()
+        p2.close()
+        a2 = s2p.update_ms_total / 1e3 / max(1, s2p.update_launches)
+        alone = {"kernel": f"k_update_s (rank-{look}, select-then-pass schedule: every SM, in place)",
+                 "avg_launch_us": a2 * 1e6, "achieved": st.bytes_per_pivot / a2 / 1e9, "peak": peak,
+                 "unit": "GB/s", "frac": st.bytes_per_pivot / a2 / 1e9 / peak,
+                 "launches_timed": s2p.update_launches}
+
     # ---- e2e: same metric through the C ABI with HOST buffers (pinned), copies inside
     Ah = torch.from_numpy(A).pin_memory()
     bh, ch = torch.from_numpy(b).pin_memory(), torch.from_numpy(c).pin_memory()
@@ -412,7 +428,7 @@ def main():
                          "pivots_per_launch": look,
                          "effective_gbs_per_pivot": st.bytes_per_pivot * pivs / (loop_ms / 1e3) / 1e9
                          if loop_ms > 0 else None,
-                         "single_pass": single},
+                         "single_pass": single, "pass_alone": alone},
             "cpu_baseline": cpu,
             "e2e": {"value": piv_e2e / (e2e_ms / 1e3), "unit": "pivots/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms": e2e_ms,
