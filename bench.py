@@ -64,7 +64,7 @@ def solver_look(lookahead, world):
     """Pivots per tableau pass the library uses (mirrors simplex_options.lookahead = 0)."""
     if lookahead > 0:
         return lookahead
-    return 16 if world == 1 else 1
+    return 16
 
 
 def reduce_max(v, world, dev):

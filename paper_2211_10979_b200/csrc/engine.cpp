@@ -159,7 +159,11 @@ struct simplex_s {
     const int q = std::max(1, S / look);
     return overlap ? (q + 1) / 2 * 2 : q;
   }
-  int kernels_per_segment() const { return look > 1 ? 2 * steps_per_segment() : S * kernels_per_pivot(); }
+  int kernels_per_segment() const {
+    if (look == 1) return S * kernels_per_pivot();
+    if (gathered()) return steps_per_segment() * nslabs * (look + 2);   // k_mlook x (look+1), pass
+    return 2 * steps_per_segment();
+  }
 
   simplex_err enter() {
     // order our stream after whatever the caller queued on its stream (e.g. inputs)
@@ -216,11 +220,11 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   if (const char* e = std::getenv("SIMPLEX_NO_LOOK_CACHE")) look_cache = !(e[0] == '1');   // experiment hook
   if (const char* e = std::getenv("SIMPLEX_FORCE_NCCL")) force_nccl = (e[0] == '1') && nranks == 1 && nslabs == 1;
   // 0 = automatic: rank-16 look-ahead on one column part, one pivot per pass otherwise
-  look = opt.lookahead > 0 ? opt.lookahead : ((nparts == 1 && !force_nccl) ? sx::kMaxLook : 1);
+  // 0 = automatic: rank-16 look-ahead (one part: pipelined with the pass; several parts: one
+  // exchange of candidate columns per selected pivot, then one pass per block)
+  look = opt.lookahead > 0 ? opt.lookahead : sx::kMaxLook;
   if (look > sx::kMaxLook) return fail(SIMPLEX_E_ARG, "lookahead larger than kMaxLook (16)");
-  if (look > 1 && (nparts > 1 || force_nccl))
-    return fail(SIMPLEX_E_ARG, "lookahead > 1 is implemented for one column part");
-  overlap = look > 1 && opt.overlap != 0;
+  overlap = look > 1 && opt.overlap != 0 && nparts == 1 && !force_nccl;
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -347,7 +351,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   // ---- exchange buffers
   xstride = roundup(m + 3, 2);
   if (gathered()) {
-    RET(dalloc(&recv, (size_t)nparts * xstride));
+    RET(dalloc(&recv, (size_t)(look > 1 ? 2 : 1) * nparts * xstride));   // look-ahead: two exchanges
     if (use_nccl()) RET(dalloc(&send, xstride));
   }
   if (use_nccl()) {
@@ -415,6 +419,26 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
 }
 
 simplex_err simplex_s::enqueue_pivot(int slot, int t) {
+  if (look > 1 && gathered()) {
+    // multi-part rank-s block: k_mlook for the block start and for every pivot on every part,
+    // each followed by the exchange of the parts' candidate columns (exchange e in buffer e&1),
+    // then the pass on every part's slab
+    double* X[2] = {recv, recv + (long long)nparts * xstride};
+    for (int u = -1; u < look; ++u) {
+      for (int sidx = 0; sidx < nslabs; ++sidx) {
+        const Slab& sl = slabs[sidx];
+        double* xout = use_nccl() ? send : X[(u + 1) & 1] + (long long)sidx * xstride;
+        CK(sx::launch_mlook(sl.v, u >= 0 ? X[u & 1] : nullptr, xout, nparts, xstride, u, look, opt.tol_opt,
+                            opt.tol_piv, sl.look_grid, stream));
+      }
+      if (use_nccl() && u + 1 < look) NK(ncclAllGather(send, X[(u + 1) & 1], (size_t)xstride, ncclFloat64, comm, stream));
+    }
+    if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
+    for (auto& sl : slabs)
+      CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
+    if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
+    return SIMPLEX_OK;
+  }
   if (look > 1) {
     const Slab& sl = slabs[0];
     if (overlap) {

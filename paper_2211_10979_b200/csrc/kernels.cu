@@ -782,6 +782,168 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   }
 }
 
+// k_mlook: rank-s look-ahead on P > 1 column parts (ranks, or virtual slabs on one GPU).
+// One launch per pivot t of a block on every part, between two exchanges of Step-1 candidates
+// carrying their chained columns (k_pack's format [v, k, col[0..m]], ONE allgather per pivot):
+//   fold the P headers -> k (lexicographic: identical on every part); the winner's column of the
+//   current tableau is in the gathered buffer; ratio test over all rows against the replicated
+//   rhs (pivot t-1 applied first) -> r (cluster argmin); colS[.][t] <- the column (replicated);
+//   own columns: row r by the chain, prow_t = row / p, R0 <- the next objective row, Step-1
+//   candidates -> cluster argmin -> this part's best column kc;
+//   the chained column kc of the next tableau (all rows) -> this part's slot for pivot t+1.
+// t == -1 (block start): R0 / RHS from T, the part's best column, its raw column -> slot for 0.
+// Every part takes the same decisions from the same gathered data, so the pivot sequence, the
+// replicated rhs / colS / basis and the status are identical everywhere; each part keeps only
+// its own columns of R0 and prowS.  The pass (k_update_s, bank 0, in place) then applies the
+// block on every part's slab.  Arithmetic and order are those of k_lookahead (bitwise).
+__global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double* __restrict__ xin,
+                                                       double* __restrict__ xout, int nparts, long long xstride,
+                                                       int t, int S, double tol_opt, double tol_piv) {
+  DevState* st = s.st;
+  __shared__ int sh_r[kMaxLook];
+  __shared__ __align__(16) Cand slot[2 * 16];
+  extern __shared__ unsigned int piv_mark[];
+  const long long gthreads = (long long)gridDim.x * blockDim.x;
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int rows = s.rows;
+  const long long ld = s.ld;
+  const int w = s.w;
+  const int pw = st->pw;
+  double* __restrict__ colS = s.colS;                 // bank 0, row stride kColS
+  double* __restrict__ prowS = s.prowS;               // bank 0, rows u = 0..15
+  double* __restrict__ R0 = s.R0;
+  double* __restrict__ RHS = s.RHS;
+  const double* __restrict__ T = s.T;
+  long long it = st->it;
+  if (t < 0 && gtid == 0) st->sb[0] = 0;             // the block is empty until a pivot is taken
+  const bool active = st->status == kRunning && it < st->stop_at;
+  if (!active) return;                                // uniform: every CTA reads the same state
+  int ph = 0;
+  Cand best = cand_none();
+  int r = -1;                                         // pivot row of step t (t >= 0)
+  if (t < 0) {
+    for (long long j = gtid; j < ld; j += gthreads) {
+      const double v = T[j];
+      R0[j] = v;
+      if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+    }
+    for (long long i = gtid; i < rows; i += gthreads) RHS[i] = T[i * ld + w];
+  } else {
+    for (int q = threadIdx.x; q < (rows + 31) / 32; q += blockDim.x) piv_mark[q] = 0u;
+    if ((int)threadIdx.x < t) sh_r[threadIdx.x] = st->rsb[0][threadIdx.x];
+    __syncthreads();
+    if ((int)threadIdx.x < t) atomicOr(&piv_mark[sh_r[threadIdx.x] >> 5], 1u << (sh_r[threadIdx.x] & 31));
+    // Step 1: fold the gathered candidates (every part the same)
+    Cand kb = cand_none();
+    int q = -1;
+    for (int p = 0; p < nparts; ++p) {
+      const double* h = xin + (long long)p * xstride;
+      const Cand c{h[0], __double_as_longlong(h[1])};
+      if (cand_less(c, kb)) { kb = c; q = p; }
+    }
+    if (kb.idx == LLONG_MAX) {                                                  // optimal
+      if (gtid == 0) st->status = kOptimal;
+      return;
+    }
+    const long long k = kb.idx;
+    const double* xcol = xin + (long long)q * xstride + 2;
+    // Step 2 over all rows; the rhs gets pivot t-1 first
+    const int r_prev = t > 0 ? st->rsb[0][t - 1] : -1;
+    const double pw_prev = t > 0 ? __ldcg(prowS + (long long)(t - 1) * ld + w) : 0.0;
+    Cand rb = cand_none();
+    for (long long i = gtid; i < rows; i += gthreads) {
+      double h = RHS[i];
+      if (t > 0) h = (i == r_prev) ? pw_prev : __fma_rn(-colS[i * kColS + t - 1], pw_prev, h);
+      RHS[i] = h;
+      const double x = xcol[i];
+      colS[i * kColS + t] = x;
+      if (i >= 1 && x > tol_piv) {
+        int basic = 0;
+        if (s.rule) basic = __ldcg(s.basis + i - 1);
+        rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, basic));
+      }
+    }
+    rb = cluster_min(rb, slot, ph);
+    ph ^= 1;
+    if (rb.idx == LLONG_MAX) {                                                  // unbounded
+      if (gtid == 0) {
+        st->status = kUnbounded;
+        st->k = (int)k;
+      }
+      return;
+    }
+    if (it >= st->cap) {                                                        // reading c12
+      if (gtid == 0) st->status = kIterLimit;
+      return;
+    }
+    r = cand_row(rb.idx);
+    const double p = xcol[r];
+    const double a0 = -xcol[0];
+    double cr[kMaxLook];
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? __ldcg(colS + (long long)r * kColS + u) : 0.0;
+    unsigned int rmask = 0u;
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u)
+      if (u < t && sh_r[u] == r) rmask |= 1u << u;
+    const double* Tr = T + (long long)r * ld;
+    double* prow = prowS + (long long)t * ld;
+    for (long long j = gtid; j < ld; j += gthreads) {
+      double x = Tr[j];
+      double pu[kMaxLook];
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? prowS[(long long)u * ld + j] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u)
+        if (u < t) x = ((rmask >> u) & 1u) ? pu[u] : __fma_rn(-cr[u], pu[u], x);
+      const double pj = __ddiv_rn(x, p);
+      prow[j] = pj;
+      const double v = __fma_rn(a0, pj, R0[j]);
+      R0[j] = v;
+      if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+    }
+    if (gtid == 0) {
+      st->rsb[0][t] = r;
+      st->sb[0] = t + 1;
+      s.basis[r - 1] = (int)k;
+      if (it < s.trace_cap) {
+        s.trace_k[it] = (int)k;
+        s.trace_r[it] = r;
+      }
+      st->it = it + 1;
+    }
+    if (threadIdx.x == 0) {
+      sh_r[t] = r;                                    // (visible after the next reduction)
+      piv_mark[r >> 5] |= 1u << (r & 31);
+    }
+    if (t + 1 >= S) return;                           // block complete: no candidate needed
+  }
+  // this part's best column for the next pivot, and that column of the next tableau
+  best = cluster_min(best, slot, ph);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    xout[0] = best.v;
+    xout[1] = __longlong_as_double(best.idx);
+  }
+  if (best.idx == LLONG_MAX) return;
+  const long long kc = best.idx - s.c0;
+  const int nu = t + 1;                               // chains applied: pivots 0..t
+  double pk[kMaxLook];
+#pragma unroll
+  for (int u = 0; u < kMaxLook; ++u) pk[u] = u < nu ? __ldcg(prowS + (long long)u * ld + kc) : 0.0;
+  for (long long i = gtid; i < rows; i += gthreads) {
+    double x = T[i * ld + kc];
+    const bool marked = (t >= 0) && ((piv_mark[i >> 5] >> (i & 31)) & 1u);
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) {
+      if (u < nu) {
+        const double cu = colS[i * kColS + u];
+        x = (marked && i == sh_r[u]) ? pk[u] : __fma_rn(-cu, pk[u], x);
+      }
+    }
+    xout[2 + i] = x;
+  }
+}
+
 // k_update_s: the rank-s pass, TMA in and TMA out.  CTA b owns column chunk c = b mod nc (cw
 // doubles, one double2 per consumer thread) and rows g, g+Gr, g+2Gr, ... (g = b div nc), so
 // all CTAs sweep Gr consecutive rows at a time: the chip-wide HBM front stays contiguous.
@@ -1115,6 +1277,7 @@ static cudaLaunchConfig_t lookahead_config(int cluster, size_t smem, cudaStream_
 int lookahead_cluster_size() {
   cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLookCacheMax);
+  cudaFuncSetAttribute(k_mlook, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const char* e = std::getenv("SIMPLEX_LOOK_CLUSTER");   // experiment hook: cap the cluster size
   const int cmax = e ? std::atoi(e) : 16;
   for (int c : {16, 8, 4, 2, 1}) {
@@ -1126,6 +1289,13 @@ int lookahead_cluster_size() {
     cudaGetLastError();
   }
   return 0;
+}
+
+cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int nparts, long long xstride, int t,
+                         int S, double tol_opt, double tol_piv, int cluster, cudaStream_t st) {
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((s.rows + 31) / 32) * sizeof(unsigned int), st, attr);
+  return cudaLaunchKernelEx(&cfg, k_mlook, s, xin, xout, nparts, xstride, t, S, tol_opt, tol_piv);
 }
 
 // Shared memory of k_lookahead: the pivot-row bitmap, plus (nqc > 0) the previous bank's chain

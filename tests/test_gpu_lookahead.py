@@ -140,3 +140,79 @@ def test_golden_8000_default_path(sx):
     assert h == int(g["tableau_hash"])
     cert = oracle.certificate(A, b, c, x, y)
     assert not cert.violations, cert.violations
+
+
+# ---- multi-part rank-s look-ahead (column slabs; k_mlook + one candidate-column exchange per
+# pivot, then one pass per slab): virtual slabs on one GPU and the real 1-rank NCCL exchange
+
+@pytest.mark.parametrize("look", [4, 16])
+@pytest.mark.parametrize("P", [2, 3, 5, 8])
+def test_multipart_dense(sx, P, look):
+    A, b, c = lpgen.dense_lp(120, 200, 77)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=look), o)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_multipart_klee_minty_and_ties(sx, P):
+    A, b, c = F.klee_minty(8)                      # repeated pivot rows inside blocks
+    o = oracle.solve(A, b, c, max_pivots=300, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, max_pivots=300, virtual_ranks=P, lookahead=16), o)
+    for seed in range(4):
+        A, b, c = F.tie_heavy(25, 31, seed)
+        A[:, A.sum(axis=0) == 0] = 1.0
+        o = oracle.solve(A, b, c, keep_tableau=True)
+        assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=8), o)
+
+
+@pytest.mark.parametrize("m,n", [(1, 9), (7, 1), (300, 40), (90, 1100)])
+def test_multipart_ragged(sx, m, n):
+    A, b, c = lpgen.dense_lp(m, n, 500 + m + n)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    P = min(3, n + m)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=16), o)
+
+
+def test_multipart_bland_and_cap(sx):
+    A, b, c = lpgen.dense_lp(60, 80, 4)
+    o = oracle.solve(A, b, c, rule=oracle.BLAND, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=3, lookahead=16, pivot_rule=sx.BLAND), o)
+    A, b, c = F.klee_minty(6)
+    o = oracle.solve(A, b, c, max_pivots=21, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=2, lookahead=8, max_pivots=21), o)
+
+
+def test_multipart_iterate_stepwise(sx):
+    A, b, c = lpgen.dense_lp(64, 64, 3)
+    with sx.Simplex(A, b, c, lookahead=8, segment_pivots=16, virtual_ranks=3) as s:
+        done_total = 0
+        for step in (1, 3, 7, 8, 2, 16, 50):
+            done, st = s.iterate(step)
+            done_total += done
+            o = oracle.solve(A, b, c, stop_after=done_total, keep_tableau=True)
+            T, _ = s.tableau()
+            assert np.array_equal(T, o.T), done_total
+            if st != sx.RUNNING:
+                break
+
+
+def test_multipart_nccl_one_rank(sx, monkeypatch):
+    """k_mlook with the captured ncclAllGather of candidate columns, 1-rank communicator."""
+    monkeypatch.setenv("SIMPLEX_FORCE_NCCL", "1")
+    A, b, c = lpgen.dense_lp(150, 230, 21)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=16), o)
+
+
+def test_multipart_golden_1000(sx):
+    g = np.load(os.path.join(GOLDEN_DIR, "dense_1000x1000_s1.npz"))
+    A, b, c = lpgen.dense_lp(1000, 1000, 1)
+    with sx.Simplex(A, b, c, virtual_ranks=4) as s:          # automatic: rank-16 look-ahead
+        st = s.solve()
+        x, y, obj, piv, _ = s.solution()
+        k, r = s.trace()
+        h = s.tableau_hash()
+    assert st == int(g["status"]) and piv == int(g["pivots"])
+    assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+    assert obj == float(g["objective"]) and np.array_equal(y, g["y"])
+    assert h == int(g["tableau_hash"])
