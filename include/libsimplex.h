@@ -92,8 +92,9 @@ typedef struct {
     int32_t  lookahead;     /* pivots applied per pass over the tableau: 1 = one pivot per pass;
                                2..16 = rank-s look-ahead blocks (select s pivots ahead from
                                chained corrections, then ONE pass applies all s — bitwise
-                               identical to s single pivots; one column part only);
-                               0 (default) = 16 on one column part, else 1                 */
+                               identical to s single pivots; on several column parts one
+                               allgather of candidate columns per selected pivot);
+                               0 (default) = 16                                            */
     int32_t  pivot_rule;    /* 0 = Dantzig (default): most negative T[0][j], lowest j / lowest
                                row on ties (readings c1-c4); 1 = Bland: first j
                                with T[0][j] < -tol_opt, ratio ties -> smallest basic-variable
