@@ -84,7 +84,14 @@ struct SlabView {
   double* R0;          // [ld]              current objective row during selection
   double* RHS;         // [rows]            current rhs column during selection
   Cand* pcand;         // [look-ahead CTAs] Step-1 candidates per CTA
+  unsigned long long* probe;   // experiment hook (SIMPLEX_PROBE): selection phase timestamps, else NULL
 };
+
+// k_lookahead phase timestamps (experiment hook): per launch slot (64), per CTA (16),
+// kProbeEv %globaltimer stamps: start, after the first reduction, then per pivot t
+// [phase A done, reduction A done, phase B done, reduction B done].
+constexpr int kProbeSlots = 64;
+constexpr int kProbeEv = 2 + 4 * kMaxLook;
 
 // Where k_select takes the entering column from.
 struct XView {

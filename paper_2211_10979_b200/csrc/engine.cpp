@@ -340,6 +340,10 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       RET(dalloc(&v.R0, v.ld));
       RET(dalloc(&v.RHS, v.rows));
       RET(dalloc(&v.pcand, sl.look_grid));
+      if (std::getenv("SIMPLEX_PROBE")) {                 // experiment hook: selection phase stamps
+        RET(dalloc(&v.probe, (size_t)sx::kProbeSlots * 16 * sx::kProbeEv));
+        CK(cudaMemset(v.probe, 0, sizeof(unsigned long long) * sx::kProbeSlots * 16 * sx::kProbeEv));
+      }
     }
   }
   RET(dalloc(&d_x, n));
@@ -657,6 +661,15 @@ simplex_err simplex_s::flush_all() {
 void simplex_s::release() {
   if (device >= 0) cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  if (const char* path = std::getenv("SIMPLEX_PROBE"))    // experiment hook: dump the stamps
+    if (!slabs.empty() && slabs[0].v.probe) {
+      std::vector<unsigned long long> hp((size_t)sx::kProbeSlots * 16 * sx::kProbeEv);
+      if (cudaMemcpy(hp.data(), slabs[0].v.probe, hp.size() * sizeof(hp[0]), cudaMemcpyDeviceToHost) == cudaSuccess)
+        if (FILE* f = std::fopen(path, "wb")) {
+          std::fwrite(hp.data(), sizeof(hp[0]), hp.size(), f);
+          std::fclose(f);
+        }
+    }
   for (auto& g : seg)
     if (g) cudaGraphExecDestroy(g);
   for (auto& v : tev)

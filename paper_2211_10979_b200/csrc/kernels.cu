@@ -600,6 +600,17 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   const long long cap = st->cap;
   const int spre = bpre >= 0 ? st->sb[bpre] : 0;
   int ph = 0;
+  unsigned long long* prb = s.probe ? s.probe + ((size_t)((it / kMaxLook) % kProbeSlots) * 16 + (blockIdx.x & 15)) * kProbeEv
+                                    : nullptr;
+#define SX_PROBE(e)                                                                 \
+  do {                                                                              \
+    if (prb && threadIdx.x == 0) {                                                  \
+      unsigned long long tnow;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));                      \
+      prb[e] = tnow;                                                                \
+    }                                                                               \
+  } while (0)
+  SX_PROBE(0);
   // nqc > 0: the previous bank's operands of this thread's columns / rows are read ONCE into
   // shared memory (the same values are chained at every step of this launch):
   //   cP[(u * nqc + q) * blockDim + tid] = prow_u[j_q],  cR[(u * nqr + q) * blockDim + tid] = col_u[i_q]
@@ -656,6 +667,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   }
   best = cluster_min(best, slot, ph);                 // (its barriers also publish piv_mark)
   ph ^= 1;
+  SX_PROBE(1);
 
   if (cache) asm volatile("cp.async.wait_group 0;" ::: "memory");   // own entries only: no barrier
   int t = 0;
@@ -705,8 +717,10 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
       if (i >= 1 && x > tol_piv)                                              // Step 2
         rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
     }
+    SX_PROBE(2 + 4 * t);
     rb = cluster_min(rb, slot, ph, T, ld);
     ph ^= 1;
+    SX_PROBE(3 + 4 * t);
     if (rb.idx == LLONG_MAX) {                                                 // unbounded
       status = kUnbounded;
       if (gtid == 0) st->k = (int)k;
@@ -770,9 +784,12 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     r_prev = r;
     c_prev = colO + t;
     p_prev = prow;
+    SX_PROBE(4 + 4 * t);
     best = cluster_min(best, slot, ph);
     ph ^= 1;
+    SX_PROBE(5 + 4 * t);
   }
+#undef SX_PROBE
   if (gtid == 0) {
     st->status = status;
     st->it = it;
