@@ -94,7 +94,10 @@ typedef struct {
                                chained corrections, then ONE pass applies all s — bitwise
                                identical to s single pivots; on several column parts one
                                allgather of candidate columns per selected pivot);
-                               0 (default) = 16                                            */
+                               17..32 = pair schedule (one column part): two selections of
+                               16 + (s-16) pivots, then ONE pass applies all s (no pipeline;
+                               pays off on tableaux whose pass dominates, 20000x40000);
+                               0 (default) = 16; > 32 -> SIMPLEX_E_ARG                     */
     int32_t  pivot_rule;    /* 0 = Dantzig (default): most negative T[0][j], lowest j / lowest
                                row on ties (readings c1-c4); 1 = Bland: first j
                                with T[0][j] < -tol_opt, ratio ties -> smallest basic-variable

@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsimplex.so")
+LIB_PATH = os.environ.get("SIMPLEX_LIB") or os.path.join(_PKG, "libsimplex.so")   # SIMPLEX_LIB: experiment variants
 
 OK = 0
 E_ARG, E_NONFINITE, E_NEG_RHS, E_OOM, E_CUDA, E_NCCL, E_STATE = -1, -2, -3, -4, -5, -6, -7

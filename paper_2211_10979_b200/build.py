@@ -56,25 +56,28 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile libsimplex.so (or, for experiments, a variant with extra -D `defines` at `out`)."""
+    if not force and not defines and out is None and up_to_date():
         return LIB
+    target = out or LIB
     inc, lib = nccl_dirs()
     ncclso = sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0]
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xptxas", "-v",
            "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
-           *SOURCES, "-o", LIB + ".tmp",
+           *["-D" + d for d in defines], *SOURCES, "-o", target + ".tmp",
            "-L", lib, "-l:" + os.path.basename(ncclso), "-Xlinker", "-rpath," + lib]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         print(res.stderr)
-    with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    if out is None:
+        with open(os.path.join(PKG, "ptxas_info.txt"), "w") as f:
+            f.write(res.stderr)
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

@@ -162,7 +162,7 @@ struct simplex_s {
   int kernels_per_segment() const {
     if (look == 1) return S * kernels_per_pivot();
     if (gathered()) return steps_per_segment() * nslabs * (look + 2);   // k_mlook x (look+1), pass
-    return 2 * steps_per_segment();
+    return (look > sx::kMaxLook ? 3 : 2) * steps_per_segment();
   }
 
   simplex_err enter() {
@@ -223,8 +223,12 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   // 0 = automatic: rank-16 look-ahead (one part: pipelined with the pass; several parts: one
   // exchange of candidate columns per selected pivot, then one pass per block)
   look = opt.lookahead > 0 ? opt.lookahead : sx::kMaxLook;
-  if (look > sx::kMaxLook) return fail(SIMPLEX_E_ARG, "lookahead larger than kMaxLook (16)");
-  overlap = look > 1 && opt.overlap != 0 && nparts == 1 && !force_nccl;
+  if (look > sx::kColS) return fail(SIMPLEX_E_ARG, "lookahead larger than 32");
+  if (look > sx::kMaxLook && nparts > 1)
+    return fail(SIMPLEX_E_ARG, "lookahead 17..32 (pair schedule) runs on one column part only");
+  // 17..32: the pair schedule — two selections (bank 0, then bank 1 chaining bank 0) and ONE
+  // pass applying both banks; select-then-pass (no pipeline)
+  overlap = look > 1 && look <= sx::kMaxLook && opt.overlap != 0 && nparts == 1 && !force_nccl;
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -289,7 +293,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       const int cwmax = 2 * sx::kThreads;
       int occ = 1;
       pass_cfg = sx::pass_cfg_choice(overlap, 16.0 * v.rows * v.ld);   // bytes read + written per pass
-      CK(sx::update_s_occupancy(pass_cfg, look, &occ, sx::update_s_smem(pass_cfg, cwmax, v.rows)));
+      CK(sx::update_s_occupancy(pass_cfg, look, &occ, sx::update_s_smem(pass_cfg, cwmax, v.rows, look)));
       if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
       const char* ps = getenv("SIMPLEX_PASS_SMS");          // experiment hook
       const long long slots = (long long)occ * (ps ? atoi(ps) : overlap ? sms - sl.look_grid : sms);
@@ -440,6 +444,18 @@ simplex_err simplex_s::enqueue_pivot(int slot, int t) {
     if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
     for (auto& sl : slabs)
       CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
+    if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
+    return SIMPLEX_OK;
+  }
+  if (look > sx::kMaxLook) {
+    // pair schedule: bank 0 selected from the tableau, bank 1 from the same tableau chaining
+    // bank 0 first (the pipeline's mode of k_lookahead), then one pass of up to 32 chains
+    const Slab& sl = slabs[0];
+    CK(sx::launch_lookahead(sl.v, sl.v.T, sx::kMaxLook, 0, -1, opt.tol_opt, opt.tol_piv, sl.look_grid, false, stream));
+    CK(sx::launch_lookahead(sl.v, sl.v.T, look - sx::kMaxLook, 1, 0, opt.tol_opt, opt.tol_piv, sl.look_grid,
+                            look_cache, stream));
+    if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
+    CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, pdl && !opt.time_kernels));
     if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
     return SIMPLEX_OK;
   }

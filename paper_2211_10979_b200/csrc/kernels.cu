@@ -508,6 +508,15 @@ __global__ void __launch_bounds__(kThreads) k_update(SlabView s, int q, double t
 // Barrier over the look-ahead kernel's CTAs: they form ONE thread-block cluster (up to 16
 // SMs), so this is the hardware cluster barrier (release/acquire at cluster scope).  Data
 // written by another CTA is read with ld.global.cg (L2), never through a stale L1.
+#ifndef SX_LOOK_RB
+#define SX_LOOK_RB 1
+#endif
+#ifndef SX_LOOK_CB
+#define SX_LOOK_CB 2
+#endif
+constexpr int kLookRB = SX_LOOK_RB;                 // rows per load batch of a selection thread
+constexpr int kLookCB = SX_LOOK_CB;                 // columns per load batch
+
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -686,36 +695,52 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     for (int u = 0; u < kMaxLook; ++u) pk[u] = u < t ? __ldcg(prowO + (long long)u * ld + k) : 0.0;
     const double pw_prev = r_prev >= 0 ? __ldcg(p_prev + w) : 0.0;
     Cand rb = cand_none();
-    int qi = 0;
-    for (long long i = gtid; i < rows; i += gthreads, ++qi) {
-      double x = T[i * ld + k];
-      double h = RHS[i];
-      double cq[kMaxLook], cu[kMaxLook];                // this row's pending-column entries
+    // rows in batches of kLookRB per thread: every load of the batch (the T entry, the rhs, the
+    // chain operands) is issued before the first dependent FMA, so a batch costs one latency
+    for (long long i0 = gtid, qi0 = 0; i0 < rows; i0 += kLookRB * gthreads, qi0 += kLookRB) {
+      double xb[kLookRB], hb[kLookRB], cpb[kLookRB], cub[kLookRB][kMaxLook];
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u)
-        cq[u] = u < spre ? (cache ? cR[((size_t)u * nqr + qi) * blockDim.x + threadIdx.x] : colP[i * kColS + u]) : 0.0;
+      for (int b = 0; b < kLookRB; ++b) {
+        const long long i = i0 + b * gthreads;
+        const bool v = b == 0 || i < rows;
+        xb[b] = v ? T[i * ld + k] : 0.0;
+        hb[b] = v ? RHS[i] : 0.0;
+        cpb[b] = v && r_prev >= 0 ? c_prev[i * kColS] : 0.0;
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) cu[u] = u < t ? colO[i * kColS + u] : 0.0;
-      if (r_prev >= 0) h = (i == r_prev) ? pw_prev : __fma_rn(-c_prev[i * kColS], pw_prev, h);
-      RHS[i] = h;
-      if ((piv_mark[i >> 5] >> (i & 31)) & 1u) {       // row i is a pivot row of a pending chain
-#pragma unroll
-        for (int u = 0; u < kMaxLook; ++u)
-          if (u < spre) x = (i == sh_rp[u]) ? qk[u] : __fma_rn(-cq[u], qk[u], x);
-#pragma unroll
-        for (int u = 0; u < kMaxLook; ++u)
-          if (u < t) x = (i == sh_r[u]) ? pk[u] : __fma_rn(-cu[u], pk[u], x);
-      } else {
-#pragma unroll
-        for (int u = 0; u < kMaxLook; ++u)
-          if (u < spre) x = __fma_rn(-cq[u], qk[u], x);
-#pragma unroll
-        for (int u = 0; u < kMaxLook; ++u)
-          if (u < t) x = __fma_rn(-cu[u], pk[u], x);
+        for (int u = 0; u < kMaxLook; ++u) cub[b][u] = v && u < t ? colO[i * kColS + u] : 0.0;
       }
-      colO[i * kColS + t] = x;
-      if (i >= 1 && x > tol_piv)                                              // Step 2
-        rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
+#pragma unroll
+      for (int b = 0; b < kLookRB; ++b) {
+        const long long i = i0 + b * gthreads;
+        if (b > 0 && i >= rows) break;
+        const long long qi = qi0 + b;
+        double x = xb[b];
+        double h = hb[b];
+        double cq[kMaxLook];                              // this row's previous-bank column entries
+#pragma unroll
+        for (int u = 0; u < kMaxLook; ++u)
+          cq[u] = u < spre ? (cache ? cR[((size_t)u * nqr + qi) * blockDim.x + threadIdx.x] : colP[i * kColS + u]) : 0.0;
+        if (r_prev >= 0) h = (i == r_prev) ? pw_prev : __fma_rn(-cpb[b], pw_prev, h);
+        RHS[i] = h;
+        if ((piv_mark[i >> 5] >> (i & 31)) & 1u) {       // row i is a pivot row of a pending chain
+#pragma unroll
+          for (int u = 0; u < kMaxLook; ++u)
+            if (u < spre) x = (i == sh_rp[u]) ? qk[u] : __fma_rn(-cq[u], qk[u], x);
+#pragma unroll
+          for (int u = 0; u < kMaxLook; ++u)
+            if (u < t) x = (i == sh_r[u]) ? pk[u] : __fma_rn(-cub[b][u], pk[u], x);
+        } else {
+#pragma unroll
+          for (int u = 0; u < kMaxLook; ++u)
+            if (u < spre) x = __fma_rn(-cq[u], qk[u], x);
+#pragma unroll
+          for (int u = 0; u < kMaxLook; ++u)
+            if (u < t) x = __fma_rn(-cub[b][u], pk[u], x);
+        }
+        colO[i * kColS + t] = x;
+        if (i >= 1 && x > tol_piv)                                              // Step 2
+          rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
+      }
     }
     SX_PROBE(2 + 4 * t);
     rb = cluster_min(rb, slot, ph, T, ld);
@@ -745,28 +770,41 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
       if (u < spre && sh_rp[u] == r) qmask |= 1u << u;
     }
     best = cand_none();
-    int qj = 0;
-    for (long long j = gtid; j < ld; j += gthreads, ++qj) {
-      double x = Tr[j];
-      const double r0 = R0[j];
-      double qu[kMaxLook], pu[kMaxLook];                // this column's pending-row entries
+    // columns in batches of kLookCB per thread (loads of the batch first, as for the rows)
+    for (long long j0 = gtid, qj0 = 0; j0 < ld; j0 += kLookCB * gthreads, qj0 += kLookCB) {
+      double xb[kLookCB], r0b[kLookCB], pub[kLookCB][kMaxLook];
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u)
-        qu[u] = u < spre ? (cache ? cP[((size_t)u * nqc + qj) * blockDim.x + threadIdx.x] : prowP[(long long)u * ld + j])
-                         : 0.0;
+      for (int b = 0; b < kLookCB; ++b) {
+        const long long j = j0 + b * gthreads;
+        const bool v = b == 0 || j < ld;
+        xb[b] = v ? Tr[j] : 0.0;
+        r0b[b] = v ? R0[j] : 0.0;
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? prowO[(long long)u * ld + j] : 0.0;
+        for (int u = 0; u < kMaxLook; ++u) pub[b][u] = v && u < t ? prowO[(long long)u * ld + j] : 0.0;
+      }
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u)
-        if (u < spre) x = ((qmask >> u) & 1u) ? qu[u] : __fma_rn(-cs[u], qu[u], x);
+      for (int b = 0; b < kLookCB; ++b) {
+        const long long j = j0 + b * gthreads;
+        if (b > 0 && j >= ld) break;
+        const long long qj = qj0 + b;
+        double x = xb[b];
+        double qu[kMaxLook];                              // this column's previous-bank row entries
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u)
-        if (u < t) x = ((rmask >> u) & 1u) ? pu[u] : __fma_rn(-cr[u], pu[u], x);
-      const double pj = __ddiv_rn(x, p);
-      prow[j] = pj;
-      const double v = __fma_rn(a0, pj, r0);
-      R0[j] = v;
-      if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));  // Step 1 of t+1
+        for (int u = 0; u < kMaxLook; ++u)
+          qu[u] = u < spre ? (cache ? cP[((size_t)u * nqc + qj) * blockDim.x + threadIdx.x] : prowP[(long long)u * ld + j])
+                           : 0.0;
+#pragma unroll
+        for (int u = 0; u < kMaxLook; ++u)
+          if (u < spre) x = ((qmask >> u) & 1u) ? qu[u] : __fma_rn(-cs[u], qu[u], x);
+#pragma unroll
+        for (int u = 0; u < kMaxLook; ++u)
+          if (u < t) x = ((rmask >> u) & 1u) ? pub[b][u] : __fma_rn(-cr[u], pub[b][u], x);
+        const double pj = __ddiv_rn(x, p);
+        prow[j] = pj;
+        const double v = __fma_rn(a0, pj, r0b[b]);
+        R0[j] = v;
+        if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));  // Step 1 of t+1
+      }
     }
     if (threadIdx.x == 0) {                             // visible after cluster_min's barriers
       sh_r[t] = r;
@@ -992,13 +1030,15 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
                                                                double* dst, int bank, int nc, int Gr, int cw) {
   pdl_launch_dependents();
   if (src == dst) pdl_wait();
+  constexpr int SC = S > kMaxLook ? kColS : kMaxLook;                // pivot-column entries staged per row
   const DevState* st = s.st;
-  const int se = st->sb[bank];
+  // S > 16: the pair schedule — bank 0 then bank 1 (chained when bank 0 is full), bank == 0
+  const int se = S > kMaxLook ? st->sb[0] + (st->sb[0] >= kMaxLook ? st->sb[1] : 0) : st->sb[bank];
   if (se == 0 && src == dst) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sT = reinterpret_cast<double*>(smem_raw);                 // [K][R][cw]
-  double* sC = sT + (size_t)K * R * cw;                              // [K][R][kMaxLook]
-  unsigned int* mark = reinterpret_cast<unsigned int*>(sC + (size_t)K * R * kMaxLook);
+  double* sC = sT + (size_t)K * R * cw;                              // [K][R][SC]
+  unsigned int* mark = reinterpret_cast<unsigned int*>(sC + (size_t)K * R * SC);
   __shared__ __align__(8) uint64_t full[K];    // stage loaded (tx bytes)
   __shared__ __align__(8) uint64_t comp[K];    // stage computed (8 consumer warps)
   __shared__ __align__(8) uint64_t empty[K];   // stage stored and free (storer)
@@ -1009,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
   const long long ld = s.ld;
   const int nwords = (rows + 31) >> 5;
   for (int i = tid; i < nwords; i += blockDim.x) mark[i] = 0u;
-  if (tid < S) sh_r[tid] = tid < se ? st->rsb[bank][tid] : -1;
+  if (tid < S) sh_r[tid] = tid < se ? (&st->rsb[0][0])[bank * kMaxLook + tid] : -1;   // rsb[2][16] flat
   if (tid == 0) {
     for (int k = 0; k < K; ++k) {
       mbar_init(&full[k], 1);
@@ -1036,13 +1076,13 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
         const int k = n % K;
         if (n >= K) mbar_wait(&empty[k], ((n / K) - 1) & 1);
         const int rin = min(R, nr - n * R);
-        mbar_arrive_expect_tx(&full[k], (uint32_t)(rin * (jn + kMaxLook) * sizeof(double)));
+        mbar_arrive_expect_tx(&full[k], (uint32_t)(rin * (jn + SC) * sizeof(double)));
         for (int rr = 0; rr < rin; ++rr) {
           const long long i = g + (long long)(n * R + rr) * Gr;
           bulk_g2s_hint(sT + ((size_t)k * R + rr) * cw, src + i * ld + j0, (uint32_t)(jn * sizeof(double)), &full[k],
                         pol);
-          bulk_g2s(sC + ((size_t)k * R + rr) * kMaxLook, s.colS + i * kColS + bank * kMaxLook,
-                   (uint32_t)(kMaxLook * sizeof(double)), &full[k]);
+          bulk_g2s(sC + ((size_t)k * R + rr) * SC, s.colS + i * kColS + bank * kMaxLook,
+                   (uint32_t)(SC * sizeof(double)), &full[k]);
         }
       }
     }
@@ -1084,7 +1124,31 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
     const int k = n % K;
     mbar_wait(&full[k], (n / K) & 1);
     const int rin = min(R, nr - n * R);
-    if (se == S && rin == R && act) {
+    if (S > kMaxLook && se == S && rin == R && act) {
+      // pair schedule, full block, full stage: as below, the pivot-column entries loaded per
+      // pair of pivots (the register file holds the 32 prow_u double2 already)
+      double2 v[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) v[rr] = *reinterpret_cast<const double2*>(sT + ((size_t)k * R + rr) * cw + jl);
+#pragma unroll
+      for (int h = 0; h < S / 2; ++h) {
+        double2 ca[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) ca[rr] = reinterpret_cast<const double2*>(sC + ((size_t)k * R + rr) * SC)[h];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          v[rr].x = __fma_rn(-ca[rr].x, pr[2 * h].x, v[rr].x);
+          v[rr].y = __fma_rn(-ca[rr].x, pr[2 * h].y, v[rr].y);
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          v[rr].x = __fma_rn(-ca[rr].y, pr[2 * h + 1].x, v[rr].x);
+          v[rr].y = __fma_rn(-ca[rr].y, pr[2 * h + 1].y, v[rr].y);
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) *reinterpret_cast<double2*>(sT + ((size_t)k * R + rr) * cw + jl) = v[rr];
+    } else if (S <= kMaxLook && se == S && rin == R && act) {
       // full block, full stage: the R rows' 2R chains interleave (independent FMAs); the
       // stage's pivot-column entries are loaded ahead of the chains
       double2 v[R];
@@ -1094,7 +1158,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
         v[rr] = *reinterpret_cast<const double2*>(sT + ((size_t)k * R + rr) * cw + jl);
 #pragma unroll
         for (int h = 0; h < S / 2; ++h)
-          ca[rr][h] = reinterpret_cast<const double2*>(sC + ((size_t)k * R + rr) * kMaxLook)[h];
+          ca[rr][h] = reinterpret_cast<const double2*>(sC + ((size_t)k * R + rr) * SC)[h];
       }
 #pragma unroll
       for (int h = 0; h < S / 2; ++h) {
@@ -1114,7 +1178,7 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
     } else if (act) {
       for (int rr = 0; rr < rin; ++rr) {
         double2 v = *reinterpret_cast<const double2*>(sT + ((size_t)k * R + rr) * cw + jl);
-        const double* cc = sC + ((size_t)k * R + rr) * kMaxLook;
+        const double* cc = sC + ((size_t)k * R + rr) * SC;
 #pragma unroll
         for (int u = 0; u < S; ++u) {
           if (u < se) {
@@ -1339,9 +1403,9 @@ cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown
 
 // k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
 // Measured (scripts/pipe_sweep.sh): {4, 12} is the fastest pass on its own.  When the pass is
-// about as long as the concurrent look-ahead selection (tableaux up to a few GB: 2 GB at 8000^2)
-// the gentler {2, 16} gives the shorter pipelined block, because it slows the selection's
-// dependent HBM reads less; a larger tableau makes the pass the critical path again.
+// shorter than the concurrent look-ahead selection (4000^2) the gentle {2, 16} gives the shorter
+// pipelined block, because it slows the selection's dependent HBM reads least; when the two are
+// about as long (2 GB at 8000^2) {6, 7} does; a larger tableau makes the pass the critical path.
 // SIMPLEX_PASS_CFG overrides the choice (experiments).
 struct PassCfg { int R, K; };
 static const PassCfg kPassCfgs[] = {{4, 12}, {4, 10}, {8, 5}, {6, 7}, {2, 16}, {4, 8}};
@@ -1349,13 +1413,16 @@ int pass_cfg_choice(bool pipelined, double pass_bytes) {
   const char* e = std::getenv("SIMPLEX_PASS_CFG");
   const int v = e ? std::atoi(e) : -1;
   if (v >= 0 && v < 6) return v;
-  return (pipelined && pass_bytes < 4e9) ? 4 : 0;
+  if (pipelined && pass_bytes < 1e9) return 4;     // selection-bound (4000^2: 210 us blocks, 104 us pass)
+  if (pipelined && pass_bytes < 4e9) return 3;     // balanced (8000^2: 370 us blocks vs 381 with {2, 16})
+  return 0;
 }
-int update_s_max(int S) { return S <= 4 ? 4 : S <= 8 ? 8 : 16; }
+int update_s_max(int S) { return S <= 4 ? 4 : S <= 8 ? 8 : S <= kMaxLook ? kMaxLook : kColS; }
 
-size_t update_s_smem(int cfg, int cw, int rows) {
+size_t update_s_smem(int cfg, int cw, int rows, int S) {
   const PassCfg c = kPassCfgs[cfg];
-  return (size_t)c.K * c.R * (cw + kMaxLook) * sizeof(double) + (size_t)((rows + 31) / 32) * sizeof(unsigned int);
+  const int sc = S > kMaxLook ? kColS : kMaxLook;
+  return (size_t)c.K * c.R * (cw + sc) * sizeof(double) + (size_t)((rows + 31) / 32) * sizeof(unsigned int);
 }
 
 template <int S, int R, int K>
@@ -1371,6 +1438,7 @@ static cudaError_t pass_prepare_s(int S, size_t smem, int* occ) {
   switch (update_s_max(S)) {
     case 4: return pass_prepare<4, R, K>(smem, occ);
     case 8: return pass_prepare<8, R, K>(smem, occ);
+    case kColS: return pass_prepare<kColS, R, K>(smem, occ);
     default: return pass_prepare<16, R, K>(smem, occ);
   }
 }
@@ -1393,13 +1461,14 @@ static cudaError_t pass_launch(const SlabView& s, int S, const double* src, doub
   switch (update_s_max(S)) {
     case 4: return launch_ex(k_update_s<4, R, K>, grid, kThreads + 64, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
     case 8: return launch_ex(k_update_s<8, R, K>, grid, kThreads + 64, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
+    case kColS: return launch_ex(k_update_s<kColS, R, K>, grid, kThreads + 64, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
     default: return launch_ex(k_update_s<16, R, K>, grid, kThreads + 64, smem, st, pdl, s, src, dst, bank, nc, Gr, cw);
   }
 }
 
 cudaError_t launch_update_s(int cfg, const SlabView& s, int S, const double* src, double* dst, int bank, int nc,
                             int Gr, int cw, cudaStream_t st, bool pdl) {
-  const size_t smem = update_s_smem(cfg, cw, s.rows);
+  const size_t smem = update_s_smem(cfg, cw, s.rows, S);
   switch (cfg) {
     case 1: return pass_launch<4, 10>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);
     case 2: return pass_launch<8, 5>(s, S, src, dst, bank, nc, Gr, cw, smem, st, pdl);

@@ -31,7 +31,7 @@ cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int
 int lookahead_cluster_size();
 int update_s_max(int S);
 int pass_cfg_choice(bool pipelined, double pass_bytes);   // k_update_s configuration (R rows x K stages)
-size_t update_s_smem(int cfg, int cw, int rows);
+size_t update_s_smem(int cfg, int cw, int rows, int S);
 cudaError_t update_s_occupancy(int cfg, int S, int* blocks_per_sm, size_t smem);
 // k_update_s: apply the pivots of chain bank `bank` to src, writing dst (src == dst: in place)
 cudaError_t launch_update_s(int cfg, const SlabView& s, int S, const double* src, double* dst, int bank, int nc,

@@ -15,8 +15,8 @@ from test_gpu_parity import GOLDEN_DIR, assert_same, gpu_solve
 pytestmark = pytest.mark.gpu
 
 PATHS = [dict(lookahead=1), dict(lookahead=4), dict(lookahead=16), dict(lookahead=16, overlap=False),
-         dict(lookahead=1, virtual_ranks=3)]
-PATH_IDS = ["pass1", "look4", "look16", "look16serial", "slabs3"]
+         dict(lookahead=32), dict(lookahead=1, virtual_ranks=3)]
+PATH_IDS = ["pass1", "look4", "look16", "look16serial", "pair32", "slabs3"]
 
 
 @pytest.fixture(scope="module")

@@ -9,8 +9,9 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-PATHS = [dict(lookahead=1), dict(lookahead=4), dict(lookahead=16), dict(lookahead=16, overlap=False)]
-PATH_IDS = ["pass1", "look4", "look16", "look16serial"]
+PATHS = [dict(lookahead=1), dict(lookahead=4), dict(lookahead=16), dict(lookahead=16, overlap=False),
+         dict(lookahead=32)]
+PATH_IDS = ["pass1", "look4", "look16", "look16serial", "pair32"]
 
 
 @pytest.fixture(scope="module")
