@@ -318,7 +318,9 @@ def main():
     # ---- roofline pass: the same solve with CUDA events around every k_update launch
     # (event-record nodes in the captured graph, on the stream the kernel runs on).  Kept
     # out of the value steps because an event node between two pivot kernels disables the
-    # programmatic-dependent-launch edge the production loop uses.
+    # programmatic-dependent-launch edge the production loop uses.  The pipelined rank-s pass
+    # is timed on the device instead (globaltimer in the kernel, the production launch
+    # sequence), because event nodes would serialize it after the concurrent selection.
     prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule,
                       overlap=not args.no_overlap)
     barrier()
@@ -423,7 +425,11 @@ def main():
                          "bytes_per_launch": st.bytes_per_pivot,
                          "bytes_formula": "16*(m+1)*(local columns incl. rhs) per pivot",
                          "avg_launch_us": avg_upd_s * 1e6, "launches_timed": upd_launches,
-                         "timed_window": f"first {window} pivots of the same solve, events per launch",
+                         "timed_window": (f"first {window} pivots of the same solve; each pass launch timed on the "
+                                          "device (%globaltimer, first CTA start -> last CTA end) while the "
+                                          "selection of the next block runs next to it")
+                         if look > 1 and not args.no_overlap else
+                         f"first {window} pivots of the same solve, CUDA events per launch",
                          "update_share_of_loop": upd_ms / prof_loop_ms if prof_loop_ms > 0 else None,
                          "pivots_per_launch": look,
                          "effective_gbs_per_pivot": st.bytes_per_pivot * pivs / (loop_ms / 1e3) / 1e9

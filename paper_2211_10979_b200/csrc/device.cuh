@@ -54,6 +54,12 @@ struct alignas(16) DevState {
   int pw;              // columns priced (local): all non-rhs in Phase I, no artificials after
   int sb[2];           // look-ahead: pivots selected into chain bank 0 / 1
   int rsb[2][kMaxLook];// look-ahead: their pivot rows, in order
+  // pass timer (SlabView::time_pass): %globaltimer of the first CTA start / last CTA end of the
+  // running k_update_s launch, CTAs finished, and the sum / count of launch durations
+  unsigned long long pass_t0, pass_t1;
+  unsigned int pass_done;
+  long long pass_n;
+  double pass_ns;
 };
 
 struct SlabView {
@@ -85,6 +91,9 @@ struct SlabView {
   double* RHS;         // [rows]            current rhs column during selection
   Cand* pcand;         // [look-ahead CTAs] Step-1 candidates per CTA
   unsigned long long* probe;   // experiment hook (SIMPLEX_PROBE): selection phase timestamps, else NULL
+  int time_pass;       // 1: k_update_s times itself on the device (DevState pass_*) — the way to
+                       // time the pipelined pass WHILE the selection runs next to it (event nodes
+                       // between the two kernels would serialize them)
 };
 
 // k_lookahead phase timestamps (experiment hook): per launch slot (64), per CTA (16),

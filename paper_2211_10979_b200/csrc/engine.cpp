@@ -154,6 +154,10 @@ struct simplex_s {
   int kernels_per_pivot() const { return nslabs * (2 + (gathered() ? 1 : 0)); }
   // graph steps per segment; the pipeline alternates two tableau buffers, so an even count
   // brings the tableau back to buffer 0 at every segment boundary
+  bool time_pass() const {                     // the pipelined pass is timed on the device
+    static const bool time_sel = std::getenv("SIMPLEX_TIME_SELECT") != nullptr;
+    return opt.time_kernels && overlap && !time_sel;
+  }
   int steps_per_segment() const {
     if (look == 1) return S;
     const int q = std::max(1, S / look);
@@ -344,6 +348,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       RET(dalloc(&v.R0, v.ld));
       RET(dalloc(&v.RHS, v.rows));
       RET(dalloc(&v.pcand, sl.look_grid));
+      v.time_pass = time_pass() ? 1 : 0;
       if (std::getenv("SIMPLEX_PROBE")) {                 // experiment hook: selection phase stamps
         RET(dalloc(&v.probe, (size_t)sx::kProbeSlots * 16 * sx::kProbeEv));
         CK(cudaMemset(v.probe, 0, sizeof(unsigned long long) * sx::kProbeSlots * 16 * sx::kProbeEv));
@@ -469,6 +474,14 @@ simplex_err simplex_s::enqueue_pivot(int slot, int t) {
       const int q = t & 1;
       double* buf[2] = {sl.v.T, sl.T2};
       static const bool time_sel = std::getenv("SIMPLEX_TIME_SELECT") != nullptr;   // experiment hook
+      if (opt.time_kernels && !time_sel) {
+        // the pass times itself on the device (SlabView::time_pass) so that it still runs
+        // concurrently with the selection: the production launch sequence, no event nodes
+        CK(sx::launch_lookahead(sl.v, buf[q], look, q ^ 1, q, opt.tol_opt, opt.tol_piv, sl.look_grid, look_cache,
+                                stream));
+        CK(sx::launch_update_s(pass_cfg, sl.v, look, buf[q], buf[q ^ 1], q, sl.nc, sl.Gr, sl.cw, stream, pdl));
+        return SIMPLEX_OK;
+      }
       if (opt.time_kernels && time_sel) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
       CK(sx::launch_lookahead(sl.v, buf[q], look, q ^ 1, q, opt.tol_opt, opt.tol_piv, sl.look_grid, look_cache, stream));
       if (opt.time_kernels)
@@ -581,7 +594,10 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
       const sx::DevState hs = h_state[slot];
       ++completed;
       const long long piv = hs.it - seen;
-      if (opt.time_kernels) {
+      if (opt.time_kernels && time_pass()) {            // device-side pass timer (cumulative)
+        upd_ms = hs.pass_ns / 1e6;
+        upd_launches = hs.pass_n;
+      } else if (opt.time_kernels) {
         const long long passes = look > 1 ? (piv + look - 1) / look : piv;   // k_update launches that did work
         for (long long q = 0; q < passes && q < steps_per_segment(); ++q) {
           float ms = 0.f;

@@ -208,6 +208,11 @@ __global__ void k_init_state(SlabView s, long long n, long long cap) {
     st->ticket2 = 0;
     st->sb[0] = 0;
     st->sb[1] = 0;
+    st->pass_t0 = ~0ull;
+    st->pass_t1 = 0ull;
+    st->pass_done = 0u;
+    st->pass_n = 0;
+    st->pass_ns = 0.0;
     st->phase = s.arts > 0 ? 1 : 2;
     st->pw = s.w;                                  // Phase I prices every non-rhs column
   }
@@ -1025,11 +1030,15 @@ __device__ __forceinline__ void bulk_s2g_hint(void* dst, const void* src, uint32
                : "memory");
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int S, int R, int K>
-__global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const double* __restrict__ src,
-                                                               double* dst, int bank, int nc, int Gr, int cw) {
-  pdl_launch_dependents();
-  if (src == dst) pdl_wait();
+__device__ __forceinline__ void update_s_body(const SlabView& s, const double* __restrict__ src, double* dst,
+                                              int bank, int nc, int Gr, int cw) {
   constexpr int SC = S > kMaxLook ? kColS : kMaxLook;                // pivot-column entries staged per row
   const DevState* st = s.st;
   // S > 16: the pair schedule — bank 0 then bank 1 (chained when bank 0 is full), bank == 0
@@ -1216,6 +1225,32 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
       }
     }
     *reinterpret_cast<double2*>(dst + (long long)r * ld + j) = v;
+  }
+}
+
+template <int S, int R, int K>
+__global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const double* __restrict__ src,
+                                                               double* dst, int bank, int nc, int Gr, int cw) {
+  pdl_launch_dependents();
+  if (src == dst) pdl_wait();
+  DevState* st = s.st;
+  const bool timed = s.time_pass && (src != dst || st->sb[bank] > 0);
+  if (timed && threadIdx.x == 0) atomicMin(&st->pass_t0, globaltimer());
+  update_s_body<S, R, K>(s, src, dst, bank, nc, Gr, cw);
+  if (!timed) return;
+  __syncthreads();                                    // every role of this CTA is done
+  if (threadIdx.x == 0) {
+    atomicMax(&st->pass_t1, globaltimer());
+    __threadfence();
+    if (atomicAdd(&st->pass_done, 1u) == gridDim.x - 1) {   // last CTA: one launch duration
+      __threadfence();
+      const unsigned long long t0 = atomicAdd(&st->pass_t0, 0ull), t1 = atomicAdd(&st->pass_t1, 0ull);
+      st->pass_ns += (double)(t1 - t0);
+      st->pass_n += 1;
+      st->pass_t0 = ~0ull;
+      st->pass_t1 = 0ull;
+      st->pass_done = 0u;
+    }
   }
 }
 
