@@ -519,6 +519,17 @@ __global__ void __launch_bounds__(kThreads) k_update(SlabView s, int q, double t
 #ifndef SX_LOOK_CB
 #define SX_LOOK_CB 2
 #endif
+// Cross-CTA reads in k_lookahead (values another CTA wrote before the last cluster barrier,
+// whose acquire invalidates L1): through L1 (default) — the 8 warps of a CTA then share one
+// L2 fetch of each broadcast operand (4000^2 blocks 211 -> 199 us) — or L2-only (SX_LOOK_CG).
+// Previous-bank operands were written by the previous launch: read-only here (nc path).
+#ifdef SX_LOOK_CG
+#define SX_LDX(p) __ldcg(p)
+#define SX_LDP(p) __ldcg(p)
+#else
+#define SX_LDX(p) (*(p))
+#define SX_LDP(p) __ldg(p)
+#endif
 constexpr int kLookRB = SX_LOOK_RB;                 // rows per load batch of a selection thread
 constexpr int kLookCB = SX_LOOK_CB;                 // columns per load batch
 
@@ -695,10 +706,10 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     // ---- phase A: rows
     double qk[kMaxLook], pk[kMaxLook];                  // prow_u[k] of both banks (L2, same for all rows)
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) qk[u] = u < spre ? __ldcg(prowP + (long long)u * ld + k) : 0.0;
+    for (int u = 0; u < kMaxLook; ++u) qk[u] = u < spre ? SX_LDP(prowP + (long long)u * ld + k) : 0.0;
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) pk[u] = u < t ? __ldcg(prowO + (long long)u * ld + k) : 0.0;
-    const double pw_prev = r_prev >= 0 ? __ldcg(p_prev + w) : 0.0;
+    for (int u = 0; u < kMaxLook; ++u) pk[u] = u < t ? SX_LDX(prowO + (long long)u * ld + k) : 0.0;
+    const double pw_prev = r_prev >= 0 ? SX_LDX(p_prev + w) : 0.0;
     Cand rb = cand_none();
     // rows in batches of kLookRB per thread: every load of the batch (the T entry, the rhs, the
     // chain operands) is issued before the first dependent FMA, so a batch costs one latency
@@ -761,11 +772,11 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     // ---- phase B: columns (pivot row, normalized; the next objective row)
     double cr[kMaxLook], cs[kMaxLook];                  // col_u[r] of both banks (L2, same for all columns)
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) cs[u] = u < spre ? __ldcg(colP + (long long)r * kColS + u) : 0.0;
+    for (int u = 0; u < kMaxLook; ++u) cs[u] = u < spre ? SX_LDP(colP + (long long)r * kColS + u) : 0.0;
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? __ldcg(colO + (long long)r * kColS + u) : 0.0;
-    const double p = __ldcg(colO + (long long)r * kColS + t);
-    const double a0 = -__ldcg(colO + t);                                      // col_t[0]
+    for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? SX_LDX(colO + (long long)r * kColS + u) : 0.0;
+    const double p = SX_LDX(colO + (long long)r * kColS + t);
+    const double a0 = -SX_LDX(colO + t);                                      // col_t[0]
     const double* Tr = T + (long long)r * ld;
     double* prow = prowO + (long long)t * ld;
     unsigned int rmask = 0u, qmask = 0u;                // bit u: r was pivot row u (own / previous bank)
