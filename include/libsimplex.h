@@ -88,7 +88,9 @@ typedef struct {
                                flow without NCCL); requires nranks == 1                    */
     int32_t  segment_pivots;/* pivots per captured CUDA-graph segment (<= 0: automatic)    */
     int32_t  time_kernels;  /* 1: record CUDA events around every pivot-update launch
-                               (see simplex_get_stats)                                     */
+                               (see simplex_get_stats); the pipelined rank-s pass is timed
+                               on the device instead (%globaltimer, first CTA start to
+                               last CTA end), so it still overlaps the selection          */
     int32_t  lookahead;     /* pivots applied per pass over the tableau: 1 = one pivot per pass;
                                2..16 = rank-s look-ahead blocks (select s pivots ahead from
                                chained corrections, then ONE pass applies all s — bitwise
@@ -117,7 +119,7 @@ typedef struct {
 typedef struct {
     int64_t pivots;              /* pivots performed so far                                  */
     int64_t update_launches;     /* timed pivot-update (K3) launches                         */
-    double  update_ms_total;     /* sum of their CUDA-event durations (time_kernels = 1)     */
+    double  update_ms_total;     /* sum of their durations (time_kernels = 1)                */
     double  loop_ms_total;       /* CUDA-event time of the device iteration loop             */
     int64_t graph_launches;      /* CUDA-graph segment launches                              */
     int64_t kernel_launches;     /* kernels of this library launched by the loop so far      */
