@@ -411,7 +411,7 @@ def main():
                                     "(two tableau buffers)" if look > 1 and not args.no_overlap else
                                     "select, then pass" if look > 1 else "one pivot per pass"),
                        "time_to_solve_ms": total_ms / args.steps,
-                       "parallelism": f"column slabs x{world}" + (" (NCCL allgather/pivot)" if world > 1 else ""),
+                       "parallelism": f"column slabs x{world}" + (" (candidate columns exchanged over peer memory per pivot)" if world > 1 else ""),
                        "l2": ("tableau %.2f GB > L2 %d MB: inputs larger than L2" % (tableau_bytes / 1e9, l2 >> 20))
                        if flush is None else "L2 flushed (write 2xL2) before every timed step",
                        "step": "reset (build Table I from device-resident A,b,c) + solve + extract"},

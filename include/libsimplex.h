@@ -114,6 +114,15 @@ typedef struct {
                                two tableau buffers (2x the tableau's HBM; falls back to 0
                                when 2.2x the tableau exceeds the free device memory); 0:
                                select, then pass, in place.  Bitwise identical results.    */
+    int32_t  exchange;      /* multi-part rank-s look-ahead (nranks > 1 or virtual_ranks > 1):
+                               0 (default) = on several ranks, peer memory when every peer
+                               GPU is reachable (k_mlook stores its candidate column straight
+                               into every rank's gather buffer over NVLink via CUDA IPC and
+                               releases a flag there — no collective launch per pivot), else
+                               NCCL; on virtual slabs, plain stores into the shared buffer;
+                               1 = one ncclAllGather per selected pivot (virtual slabs: plain
+                               stores); 2 = the peer-memory protocol (also on virtual slabs:
+                               its test path) or SIMPLEX_E_CUDA.  Bitwise identical results. */
 } simplex_options;
 
 typedef struct {

@@ -44,7 +44,8 @@ class Options(C.Structure):
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_void_p),
                 ("stream", C.c_void_p), ("virtual_ranks", C.c_int32), ("segment_pivots", C.c_int32),
                 ("time_kernels", C.c_int32), ("lookahead", C.c_int32),
-                ("pivot_rule", C.c_int32), ("phase1", C.c_int32), ("overlap", C.c_int32)]
+                ("pivot_rule", C.c_int32), ("phase1", C.c_int32), ("overlap", C.c_int32),
+                ("exchange", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -172,7 +173,7 @@ class Simplex:
 
     def __init__(self, A, b, c, *, tol_opt=1e-7, tol_piv=1e-10, max_pivots=0, record_trace=True,
                  device=None, group=None, virtual_ranks=1, segment_pivots=0, time_kernels=False,
-                 lookahead=0, pivot_rule=DANTZIG, phase1=True, overlap=True, stream=None):
+                 lookahead=0, pivot_rule=DANTZIG, phase1=True, overlap=True, stream=None, exchange=0):
         L = lib()
         m, n = (int(A.shape[0]), int(A.shape[1]))
         o = default_options()
@@ -186,6 +187,7 @@ class Simplex:
         o.pivot_rule = int(pivot_rule)
         o.phase1 = 1 if phase1 else 0
         o.overlap = 1 if overlap else 0
+        o.exchange = int(exchange)
         s = stream if stream is not None else _current_stream()
         o.stream = s if s else None
         self._idbuf = None

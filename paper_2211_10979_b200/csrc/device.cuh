@@ -60,6 +60,25 @@ struct alignas(16) DevState {
   unsigned int pass_done;
   long long pass_n;
   double pass_ns;
+  // multi-part look-ahead over peer memory: exchanges this part has published (monotone over
+  // the handle's life, never reset; every part counts the same)
+  unsigned long long xseq;
+};
+
+// Destinations of a part's exchange slot in the peer-memory exchange of k_mlook.
+// Every value travels as two 8-byte words {32 data bits, 32-bit sequence number} (the "LL"
+// format: an aligned 8-byte store is single-copy atomic, so a reader that sees the expected
+// sequence number in a word also sees that word's data) — no fence, no flag, no barrier: the
+// writer stores its slot [v, k, col[0..m]] straight into buffer (t+1)&1 of EVERY rank's gather
+// buffer (a peer's through its CUDA-IPC mapping, over NVLink) and each reader polls exactly the
+// words it consumes.  Gather buffer: 2 parities x nparts slots x xstride values x 2 words.
+constexpr int kMaxPeers = 8;
+struct XPeers {
+  int n;                               // destination ranks; 0 = exchange outside the kernel
+  int part;                            // this part's slot index in every gather buffer
+  long long half;                      // values per parity (nparts * xstride)
+  unsigned long long* x[kMaxPeers];    // gather buffers of every rank (LL words)
+  const unsigned long long* mine;      // this rank's gather buffer
 };
 
 struct SlabView {

@@ -55,6 +55,7 @@ simplex_err fail(simplex_err code, const std::string& msg) {
   } while (0)
 
 long long roundup(long long a, long long b) { return (a + b - 1) / b * b; }
+constexpr int kMaxPeersHost = sx::kMaxPeers;
 
 struct Slab {
   sx::SlabView v{};
@@ -102,6 +103,10 @@ struct simplex_s {
   double* send = nullptr;
   double* recv = nullptr;
   long long xstride = 0;
+  bool p2p = false;                     // multi-part look-ahead exchanges over peer memory (no NCCL)
+  unsigned long long* xll = nullptr;    // peer-memory gather buffer (LL words, device.cuh XPeers)
+  std::vector<void*> ipc_open;          // peer allocations mapped with cudaIpcOpenMemHandle
+  std::vector<sx::XPeers> xpeers;       // per slab
   // extraction scratch
   double* d_x = nullptr;
   double* d_y = nullptr;
@@ -185,6 +190,7 @@ struct simplex_s {
   simplex_err run(long long max_pivots, long long* done);
   simplex_err flush_all();
   void release();
+  simplex_err setup_p2p();
 };
 
 // Rows with b_i < 0 (1-based, ascending) and their artificial index (reading p1).
@@ -233,6 +239,13 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   // 17..32: the pair schedule — two selections (bank 0, then bank 1 chaining bank 0) and ONE
   // pass applying both banks; select-then-pass (no pipeline)
   overlap = look > 1 && look <= sx::kMaxLook && opt.overlap != 0 && nparts == 1 && !force_nccl;
+  if (opt.exchange < 0 || opt.exchange > 2) return fail(SIMPLEX_E_ARG, "exchange must be 0, 1 or 2");
+  // multi-part look-ahead on several ranks: peer-memory exchange unless NCCL is asked for
+  // (peer reachability is checked once the device is known); the 1-rank NCCL hook keeps NCCL
+  // (one GPU, virtual slabs: only when asked for — there the protocol is pure overhead, the
+  // stream already orders the parts; measured +6 us per k_mlook launch for the system fence)
+  p2p = look > 1 && nparts > 1 && !force_nccl && (opt.exchange == 2 || (opt.exchange == 0 && nranks > 1));
+  if (p2p && nranks > kMaxPeersHost) return fail(SIMPLEX_E_ARG, "peer-memory exchange supports up to 8 ranks");
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -342,6 +355,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     RET(dalloc(&v.trace_k, std::max<long long>(v.trace_cap, 1)));
     RET(dalloc(&v.trace_r, std::max<long long>(v.trace_cap, 1)));
     RET(dalloc(&v.st, 1));
+    CK(cudaMemsetAsync(v.st, 0, sizeof(sx::DevState), stream));   // xseq starts at 0 (never reset)
     if (look > 1) {
       RET(dalloc(&v.colS, (size_t)v.rows * sx::kColS));
       RET(dalloc(&v.prowS, (size_t)sx::kColS * v.ld));
@@ -365,7 +379,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   xstride = roundup(m + 3, 2);
   if (gathered()) {
     RET(dalloc(&recv, (size_t)(look > 1 ? 2 : 1) * nparts * xstride));   // look-ahead: two exchanges
-    if (use_nccl()) RET(dalloc(&send, xstride));
+    if (use_nccl() && !p2p) RET(dalloc(&send, xstride));
   }
   if (use_nccl()) {
     ncclUniqueId id;
@@ -376,6 +390,86 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       NK(ncclGetUniqueId(&id));
     }
     NK(ncclCommInitRank(&comm, nranks, id, rank));
+  }
+  if (p2p) RET(setup_p2p());
+  return SIMPLEX_OK;
+}
+
+// Peer-memory exchange of the multi-part look-ahead: every part's k_mlook stores
+// its slot, as sequence-numbered LL words, straight into every rank's gather buffer.  Ranks map
+// each other's gather buffer through CUDA IPC; the handles travel over NCCL once.  Falls back to
+// the NCCL allgather (exchange = 0) when a peer is not reachable.
+simplex_err simplex_s::setup_p2p() {
+  const long long half = (long long)nparts * xstride;
+  RET(dalloc(&xll, (size_t)(2 * 2 * half)));                            // 2 parities x 2 words per value
+  CK(cudaMemsetAsync(xll, 0, sizeof(unsigned long long) * 2 * 2 * half, stream));   // sequence 0: never written
+  std::vector<unsigned long long*> px((size_t)nranks, xll);
+  if (nranks > 1) {
+    int ok = 1;
+    std::vector<int> devs((size_t)nranks, -1);
+    {
+      int* d_dev = nullptr;
+      RET(dalloc(&d_dev, (size_t)nranks));
+      CK(cudaMemcpyAsync(d_dev + rank, &device, sizeof(int), cudaMemcpyHostToDevice, stream));
+      NK(ncclAllGather(d_dev + rank, d_dev, 1, ncclInt32, comm, stream));
+      CK(cudaMemcpyAsync(devs.data(), d_dev, sizeof(int) * nranks, cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+    }
+    for (int r = 0; r < nranks; ++r) {
+      if (r == rank) continue;
+      int can = 0;
+      if (devs[r] == device || cudaDeviceCanAccessPeer(&can, device, devs[r]) != cudaSuccess) can = 0;
+      ok &= can;
+    }
+    cudaGetLastError();
+    // every rank must take the same decision
+    {
+      int* d_ok = nullptr;
+      RET(dalloc(&d_ok, 1));
+      CK(cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, stream));
+      NK(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, comm, stream));
+      CK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+    }
+    if (!ok) {
+      if (opt.exchange == 2) return fail(SIMPLEX_E_CUDA, "exchange = 2 (peer memory) but a peer GPU is not reachable");
+      p2p = false;
+      RET(dalloc(&send, xstride));                        // NCCL allgather path
+      return SIMPLEX_OK;
+    }
+    cudaIpcMemHandle_t hx;
+    CK(cudaIpcGetMemHandle(&hx, xll));
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    unsigned char* d_h = nullptr;
+    RET(dalloc(&d_h, hb * nranks));
+    std::vector<unsigned char> hh(hb * nranks);
+    std::memcpy(hh.data() + hb * rank, &hx, sizeof(hx));
+    CK(cudaMemcpyAsync(d_h + hb * rank, hh.data() + hb * rank, hb, cudaMemcpyHostToDevice, stream));
+    NK(ncclAllGather(d_h + hb * rank, d_h, hb, ncclUint8, comm, stream));
+    CK(cudaMemcpyAsync(hh.data(), d_h, hb * nranks, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    for (int r = 0; r < nranks; ++r) {
+      if (r == rank) continue;
+      cudaIpcMemHandle_t a;
+      std::memcpy(&a, hh.data() + hb * r, sizeof(a));
+      void* pa = nullptr;
+      CK(cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess));
+      ipc_open.push_back(pa);
+      px[(size_t)r] = static_cast<unsigned long long*>(pa);
+    }
+    // no rank may store into a peer before that peer's buffer is zeroed: the memset above is
+    // ordered before this allreduce on every rank
+    NK(ncclAllReduce(reinterpret_cast<int*>(d_h), reinterpret_cast<int*>(d_h), 1, ncclInt32, ncclMax, comm, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+  xpeers.assign((size_t)nslabs, sx::XPeers{});
+  for (int sidx = 0; sidx < nslabs; ++sidx) {
+    sx::XPeers& xp = xpeers[(size_t)sidx];
+    xp.n = nranks;
+    xp.part = rank * nslabs + sidx;
+    xp.half = half;
+    for (int r = 0; r < nranks; ++r) xp.x[r] = px[(size_t)r];
+    xp.mine = xll;
   }
   return SIMPLEX_OK;
 }
@@ -437,14 +531,16 @@ simplex_err simplex_s::enqueue_pivot(int slot, int t) {
     // each followed by the exchange of the parts' candidate columns (exchange e in buffer e&1),
     // then the pass on every part's slab
     double* X[2] = {recv, recv + (long long)nparts * xstride};
+    static const sx::XPeers no_peers{};
     for (int u = -1; u < look; ++u) {
       for (int sidx = 0; sidx < nslabs; ++sidx) {
         const Slab& sl = slabs[sidx];
-        double* xout = use_nccl() ? send : X[(u + 1) & 1] + (long long)sidx * xstride;
+        double* xout = p2p ? nullptr : use_nccl() ? send : X[(u + 1) & 1] + (long long)sidx * xstride;
         CK(sx::launch_mlook(sl.v, u >= 0 ? X[u & 1] : nullptr, xout, nparts, xstride, u, look, opt.tol_opt,
-                            opt.tol_piv, sl.look_grid, stream));
+                            opt.tol_piv, sl.look_grid, p2p ? xpeers[(size_t)sidx] : no_peers, stream));
       }
-      if (use_nccl() && u + 1 < look) NK(ncclAllGather(send, X[(u + 1) & 1], (size_t)xstride, ncclFloat64, comm, stream));
+      if (!p2p && use_nccl() && u + 1 < look)
+        NK(ncclAllGather(send, X[(u + 1) & 1], (size_t)xstride, ncclFloat64, comm, stream));
     }
     if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
     for (auto& sl : slabs)
@@ -706,6 +802,8 @@ void simplex_s::release() {
     if (g) cudaGraphExecDestroy(g);
   for (auto& v : tev)
     for (auto e : v) cudaEventDestroy(e);
+  for (void* p : ipc_open) cudaIpcCloseMemHandle(p);
+  ipc_open.clear();
   if (comm) ncclCommDestroy(comm);
   for (void* p : allocs) cudaFree(p);
   allocs.clear();
@@ -735,6 +833,7 @@ void simplex_default_options(simplex_options* o) {
   o->nccl_id = nullptr;
   o->stream = nullptr;
   o->virtual_ranks = 1;
+  o->exchange = 0;
   o->segment_pivots = 0;
   o->time_kernels = 0;
   o->lookahead = 0;

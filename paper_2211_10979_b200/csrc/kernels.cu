@@ -867,9 +867,26 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
 // replicated rhs / colS / basis and the status are identical everywhere; each part keeps only
 // its own columns of R0 and prowS.  The pass (k_update_s, bank 0, in place) then applies the
 // block on every part's slab.  Arithmetic and order are those of k_lookahead (bitwise).
+// LL words of the peer-memory exchange (device.cuh XPeers): value x with sequence number q
+__device__ __forceinline__ void ll_store(unsigned long long* w, double x, unsigned int q) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  const unsigned long long lo = ((unsigned long long)q << 32) | (b & 0xffffffffull);
+  const unsigned long long hi = ((unsigned long long)q << 32) | (b >> 32);
+  asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(w), "l"(lo), "l"(hi) : "memory");
+}
+__device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned int q) {
+  unsigned long long lo, hi;
+  for (;;) {
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(w) : "memory");
+    if ((unsigned int)(lo >> 32) == q && (unsigned int)(hi >> 32) == q) break;
+    __nanosleep(32);
+  }
+  return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+}
+
 __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double* __restrict__ xin,
                                                        double* __restrict__ xout, int nparts, long long xstride,
-                                                       int t, int S, double tol_opt, double tol_piv) {
+                                                       int t, int S, double tol_opt, double tol_piv, XPeers xp) {
   DevState* st = s.st;
   __shared__ int sh_r[kMaxLook];
   __shared__ __align__(16) Cand slot[2 * 16];
@@ -889,6 +906,14 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
   if (t < 0 && gtid == 0) st->sb[0] = 0;             // the block is empty until a pivot is taken
   const bool active = st->status == kRunning && it < st->stop_at;
   if (!active) return;                                // uniform: every CTA reads the same state
+  // peer-memory exchange: the slots of this pivot carry sequence number xseq (every part has
+  // published as many slots as this one); this launch publishes xseq + 1
+  const unsigned int xseq = xp.n > 0 ? (unsigned int)st->xseq : 0u;
+  const unsigned long long* xll = xp.n > 0 ? xp.mine + 2 * (long long)(t & 1) * xp.half : nullptr;
+  // value e of part q's slot in the gathered buffer of this pivot
+  auto xget = [&](int q, long long e) -> double {
+    return xll ? ll_load(xll + 2 * ((long long)q * xstride + e), xseq) : __ldcg(xin + (long long)q * xstride + e);
+  };
   int ph = 0;
   Cand best = cand_none();
   int r = -1;                                         // pivot row of step t (t >= 0)
@@ -908,8 +933,7 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
     Cand kb = cand_none();
     int q = -1;
     for (int p = 0; p < nparts; ++p) {
-      const double* h = xin + (long long)p * xstride;
-      const Cand c{h[0], __double_as_longlong(h[1])};
+      const Cand c{xget(p, 0), __double_as_longlong(xget(p, 1))};
       if (cand_less(c, kb)) { kb = c; q = p; }
     }
     if (kb.idx == LLONG_MAX) {                                                  // optimal
@@ -917,7 +941,6 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
       return;
     }
     const long long k = kb.idx;
-    const double* xcol = xin + (long long)q * xstride + 2;
     // Step 2 over all rows; the rhs gets pivot t-1 first
     const int r_prev = t > 0 ? st->rsb[0][t - 1] : -1;
     const double pw_prev = t > 0 ? __ldcg(prowS + (long long)(t - 1) * ld + w) : 0.0;
@@ -926,7 +949,7 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
       double h = RHS[i];
       if (t > 0) h = (i == r_prev) ? pw_prev : __fma_rn(-colS[i * kColS + t - 1], pw_prev, h);
       RHS[i] = h;
-      const double x = xcol[i];
+      const double x = xget(q, 2 + i);
       colS[i * kColS + t] = x;
       if (i >= 1 && x > tol_piv) {
         int basic = 0;
@@ -948,8 +971,8 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
       return;
     }
     r = cand_row(rb.idx);
-    const double p = xcol[r];
-    const double a0 = -xcol[0];
+    const double p = xget(q, 2 + r);
+    const double a0 = -xget(q, 2);
     double cr[kMaxLook];
 #pragma unroll
     for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? __ldcg(colS + (long long)r * kColS + u) : 0.0;
@@ -991,28 +1014,42 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
   }
   // this part's best column for the next pivot, and that column of the next tableau
   best = cluster_min(best, slot, ph);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    xout[0] = best.v;
-    xout[1] = __longlong_as_double(best.idx);
+  // slot destinations: xout (NCCL send buffer or the one-GPU gather buffer), or buffer (t+1)&1
+  // of every rank's gather buffer (peer memory)
+  const long long off = 2 * ((long long)((t + 1) & 1) * xp.half + (long long)xp.part * xstride);   // LL words
+  if (blockIdx.x == 0 && threadIdx.x < (xp.n > 0 ? xp.n : 1)) {
+    if (xp.n > 0) {
+      ll_store(xp.x[threadIdx.x] + off, best.v, xseq + 1);
+      ll_store(xp.x[threadIdx.x] + off + 2, __longlong_as_double(best.idx), xseq + 1);
+    } else {
+      xout[0] = best.v;
+      xout[1] = __longlong_as_double(best.idx);
+    }
   }
-  if (best.idx == LLONG_MAX) return;
-  const long long kc = best.idx - s.c0;
-  const int nu = t + 1;                               // chains applied: pivots 0..t
-  double pk[kMaxLook];
+  if (best.idx != LLONG_MAX) {
+    const long long kc = best.idx - s.c0;
+    const int nu = t + 1;                             // chains applied: pivots 0..t
+    double pk[kMaxLook];
 #pragma unroll
-  for (int u = 0; u < kMaxLook; ++u) pk[u] = u < nu ? __ldcg(prowS + (long long)u * ld + kc) : 0.0;
-  for (long long i = gtid; i < rows; i += gthreads) {
-    double x = T[i * ld + kc];
-    const bool marked = (t >= 0) && ((piv_mark[i >> 5] >> (i & 31)) & 1u);
+    for (int u = 0; u < kMaxLook; ++u) pk[u] = u < nu ? __ldcg(prowS + (long long)u * ld + kc) : 0.0;
+    for (long long i = gtid; i < rows; i += gthreads) {
+      double x = T[i * ld + kc];
+      const bool marked = (t >= 0) && ((piv_mark[i >> 5] >> (i & 31)) & 1u);
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) {
-      if (u < nu) {
-        const double cu = colS[i * kColS + u];
-        x = (marked && i == sh_r[u]) ? pk[u] : __fma_rn(-cu, pk[u], x);
+      for (int u = 0; u < kMaxLook; ++u) {
+        if (u < nu) {
+          const double cu = colS[i * kColS + u];
+          x = (marked && i == sh_r[u]) ? pk[u] : __fma_rn(-cu, pk[u], x);
+        }
+      }
+      if (xp.n == 0) {
+        xout[2 + i] = x;
+      } else {
+        for (int d = 0; d < xp.n; ++d) ll_store(xp.x[d] + off + 2 * (2 + i), x, xseq + 1);   // NVLink
       }
     }
-    xout[2 + i] = x;
   }
+  if (xp.n > 0 && gtid == 0) st->xseq = xseq + 1;
 }
 
 // k_update_s: the rank-s pass, TMA in and TMA out.  CTA b owns column chunk c = b mod nc (cw
@@ -1419,10 +1456,10 @@ int lookahead_cluster_size() {
 }
 
 cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int nparts, long long xstride, int t,
-                         int S, double tol_opt, double tol_piv, int cluster, cudaStream_t st) {
+                         int S, double tol_opt, double tol_piv, int cluster, const XPeers& xp, cudaStream_t st) {
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((s.rows + 31) / 32) * sizeof(unsigned int), st, attr);
-  return cudaLaunchKernelEx(&cfg, k_mlook, s, xin, xout, nparts, xstride, t, S, tol_opt, tol_piv);
+  return cudaLaunchKernelEx(&cfg, k_mlook, s, xin, xout, nparts, xstride, t, S, tol_opt, tol_piv, xp);
 }
 
 // Shared memory of k_lookahead: the pivot-row bitmap, plus (nqc > 0) the previous bank's chain

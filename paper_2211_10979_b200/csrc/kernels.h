@@ -26,8 +26,9 @@ cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown
                              double tol_piv, int cluster, bool cache, cudaStream_t st);
 size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int* nqr);
 // k_mlook: one pivot t (t = -1: block start) of the multi-part look-ahead, between two exchanges
+// xp.n > 0: the slot goes to every rank's gather buffer over peer memory + flags (no NCCL)
 cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int nparts, long long xstride, int t,
-                         int S, double tol_opt, double tol_piv, int cluster, cudaStream_t st);
+                         int S, double tol_opt, double tol_piv, int cluster, const XPeers& xp, cudaStream_t st);
 int lookahead_cluster_size();
 int update_s_max(int S);
 int pass_cfg_choice(bool pipelined, double pass_bytes);   // k_update_s configuration (R rows x K stages)

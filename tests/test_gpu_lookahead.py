@@ -145,24 +145,50 @@ def test_golden_8000_default_path(sx):
 # ---- multi-part rank-s look-ahead (column slabs; k_mlook + one candidate-column exchange per
 # pivot, then one pass per slab): virtual slabs on one GPU and the real 1-rank NCCL exchange
 
+@pytest.fixture(params=[2, 0], ids=["peer", "direct"])
+def xch(request):
+    """exchange 2: the peer-memory protocol (slot stores + released flags, waited on by the
+    next k_mlook); 0 on virtual slabs: slots written into the shared gather buffer, stream
+    order only."""
+    return request.param
+
+
 @pytest.mark.parametrize("look", [4, 16])
 @pytest.mark.parametrize("P", [2, 3, 5, 8])
-def test_multipart_dense(sx, P, look):
+def test_multipart_dense(sx, P, look, xch):
     A, b, c = lpgen.dense_lp(120, 200, 77)
     o = oracle.solve(A, b, c, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=look), o)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=look, exchange=xch), o)
 
 
 @pytest.mark.parametrize("P", [2, 4])
-def test_multipart_klee_minty_and_ties(sx, P):
+def test_multipart_klee_minty_and_ties(sx, P, xch):
     A, b, c = F.klee_minty(8)                      # repeated pivot rows inside blocks
     o = oracle.solve(A, b, c, max_pivots=300, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, max_pivots=300, virtual_ranks=P, lookahead=16), o)
+    assert_same(gpu_solve(sx, A, b, c, max_pivots=300, virtual_ranks=P, lookahead=16, exchange=xch), o)
     for seed in range(4):
         A, b, c = F.tie_heavy(25, 31, seed)
         A[:, A.sum(axis=0) == 0] = 1.0
         o = oracle.solve(A, b, c, keep_tableau=True)
-        assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=8), o)
+        assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=8, exchange=xch), o)
+
+
+def test_multipart_peer_exchange_reset_and_options(sx):
+    """The exchange counters are monotone over the handle's life: a reset and a second solve
+    reuse the flags; exchange = 2 (peer memory required) works on one GPU; bad values fail."""
+    A, b, c = lpgen.dense_lp(90, 140, 5)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    with sx.Simplex(A, b, c, virtual_ranks=3, lookahead=16, exchange=2) as s:
+        for _ in range(3):
+            st = s.solve()
+            x, y, obj, piv, _ = s.solution()
+            k, r = s.trace()
+            assert st == o.status and piv == o.pivots and obj == o.objective
+            assert np.array_equal(k, o.trace_k) and np.array_equal(r, o.trace_r)
+            assert np.array_equal(x, o.x) and np.array_equal(y, o.y)
+            s.reset(A, b, c)
+    with pytest.raises(sx.SimplexError):
+        sx.Simplex(A, b, c, virtual_ranks=2, exchange=3)
 
 
 @pytest.mark.parametrize("m,n", [(1, 9), (7, 1), (300, 40), (90, 1100)])
@@ -182,9 +208,9 @@ def test_multipart_bland_and_cap(sx):
     assert_same(gpu_solve(sx, A, b, c, virtual_ranks=2, lookahead=8, max_pivots=21), o)
 
 
-def test_multipart_iterate_stepwise(sx):
+def test_multipart_iterate_stepwise(sx, xch):
     A, b, c = lpgen.dense_lp(64, 64, 3)
-    with sx.Simplex(A, b, c, lookahead=8, segment_pivots=16, virtual_ranks=3) as s:
+    with sx.Simplex(A, b, c, lookahead=8, segment_pivots=16, virtual_ranks=3, exchange=xch) as s:
         done_total = 0
         for step in (1, 3, 7, 8, 2, 16, 50):
             done, st = s.iterate(step)
