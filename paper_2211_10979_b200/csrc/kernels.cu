@@ -44,6 +44,37 @@ __device__ __forceinline__ Cand ratio_cand(int rule, double q, long long i, int 
 }
 __device__ __forceinline__ int cand_row(long long idx) { return (int)(idx & 0xffffffffLL); }
 
+// Order-preserving map of a non-NaN double to an unsigned 64-bit key (IEEE order = unsigned
+// order); -0 and +0 get the same key, as they compare equal (reading c16).
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+  const long long b = __double_as_longlong(v == 0.0 ? 0.0 : v);
+  return b < 0 ? ~(unsigned long long)b : ((unsigned long long)b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+  return __longlong_as_double((k >> 63) ? (long long)(k & 0x7fffffffffffffffull) : (long long)~k);
+}
+
+#ifndef SX_WARP_MIN_SHFL
+// Warp-wide lexicographic argmin of (v, idx) on the 32-bit reduction unit: the 128-bit key
+// (ord_key(v), idx) is reduced one 32-bit word at a time (redux.sync.min.u32), lanes that lost
+// a word dropping out (they contribute 0xffffffff).  Equal to the pairwise cand_min fold for
+// non-NaN values (c18); idx >= 0, so unsigned order is the signed order.  Every lane returns
+// the result (v of an all-zero key comes back as +0).  Full warps only.
+__device__ __forceinline__ Cand warp_min(Cand c) {
+  const unsigned long long k = ord_key(c.v);
+  const unsigned long long ix = (unsigned long long)c.idx;
+  const unsigned int w0 = (unsigned int)(k >> 32), w1 = (unsigned int)k;
+  const unsigned int w2 = (unsigned int)(ix >> 32), w3 = (unsigned int)ix;
+  const unsigned int m0 = __reduce_min_sync(0xffffffffu, w0);
+  bool e = w0 == m0;
+  const unsigned int m1 = __reduce_min_sync(0xffffffffu, e ? w1 : 0xffffffffu);
+  e = e && w1 == m1;
+  const unsigned int m2 = __reduce_min_sync(0xffffffffu, e ? w2 : 0xffffffffu);
+  e = e && w2 == m2;
+  const unsigned int m3 = __reduce_min_sync(0xffffffffu, e ? w3 : 0xffffffffu);
+  return Cand{ord_val(((unsigned long long)m0 << 32) | m1), (long long)(((unsigned long long)m2 << 32) | m3)};
+}
+#else
 __device__ __forceinline__ Cand warp_min(Cand c) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -54,6 +85,7 @@ __device__ __forceinline__ Cand warp_min(Cand c) {
   }
   return c;
 }
+#endif
 
 // Block-wide lexicographic argmin; every thread returns the result.  Contains
 // __syncthreads(): call from block-uniform control flow only.
