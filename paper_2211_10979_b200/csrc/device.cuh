@@ -26,6 +26,8 @@ constexpr int kColS = 2 * kMaxLook;        // colS row stride / prowS rows: two 
 
 constexpr uint32_t kErrNonFinite = 1u;
 constexpr uint32_t kErrNegRhs = 2u;
+constexpr uint32_t kErrExchange = 4u;      // peer-memory exchange timed out (status -> kFault)
+constexpr int kFault = -2;                 // device loop stopped on an error (see err)
 
 // (value, index) argmin candidate; "none" = (+inf, INT64_MAX).  Compared
 // lexicographically, which equals the oracle's ascending strict-< scan when no NaN

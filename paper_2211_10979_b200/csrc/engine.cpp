@@ -702,6 +702,12 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
           ++upd_launches;
         }
       }
+      if (hs.err & sx::kErrExchange) {
+        CK(cudaStreamSynchronize(stream));
+        status = SIMPLEX_RUNNING;
+        return fail(SIMPLEX_E_NCCL, "peer-memory exchange timed out: a peer did not publish its candidate "
+                                    "column within 30 s (the handle must be destroyed)");
+      }
       seen = hs.it;
       status = hs.status;
       it = hs.it;

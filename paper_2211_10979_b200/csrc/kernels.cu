@@ -906,12 +906,27 @@ __device__ __forceinline__ void ll_store(unsigned long long* w, double x, unsign
   const unsigned long long hi = ((unsigned long long)q << 32) | (b >> 32);
   asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(w), "l"(lo), "l"(hi) : "memory");
 }
-__device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned int q) {
-  unsigned long long lo, hi;
-  for (;;) {
+// Polls until both words carry sequence number q.  A peer that never publishes (a dead rank)
+// must not hang the GPU: after 30 s the word is given up on, the handle's loop is stopped
+// (status kFault, err kErrExchange) and the host reports SIMPLEX_E_NCCL.
+__device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned int q, DevState* st) {
+  unsigned long long lo, hi, t0 = 0;
+  for (unsigned int n = 0;; ++n) {
     asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(w) : "memory");
     if ((unsigned int)(lo >> 32) == q && (unsigned int)(hi >> 32) == q) break;
     __nanosleep(32);
+    if ((n & 1023u) == 1023u) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (*(volatile int*)&st->status == kFault) return 0.0;     // another thread gave up already
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > 30000000000ull) {
+        atomicOr(&st->err, kErrExchange);
+        st->status = kFault;
+        return 0.0;
+      }
+    }
   }
   return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
 }
@@ -944,7 +959,7 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
   const unsigned long long* xll = xp.n > 0 ? xp.mine + 2 * (long long)(t & 1) * xp.half : nullptr;
   // value e of part q's slot in the gathered buffer of this pivot
   auto xget = [&](int q, long long e) -> double {
-    return xll ? ll_load(xll + 2 * ((long long)q * xstride + e), xseq) : __ldcg(xin + (long long)q * xstride + e);
+    return xll ? ll_load(xll + 2 * ((long long)q * xstride + e), xseq, st) : __ldcg(xin + (long long)q * xstride + e);
   };
   int ph = 0;
   Cand best = cand_none();
