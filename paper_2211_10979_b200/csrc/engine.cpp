@@ -104,6 +104,10 @@ struct simplex_s {
   double* recv = nullptr;
   long long xstride = 0;
   bool p2p = false;                     // multi-part look-ahead exchanges over peer memory (no NCCL)
+  bool mblock = false;                  // ... with the whole block's selection in one k_mblock launch
+  std::vector<cudaStream_t> xs;         // virtual slabs under k_mblock: one stream each (co-resident)
+  cudaEvent_t ev_fork = nullptr;
+  std::vector<cudaEvent_t> ev_join;
   unsigned long long* xll = nullptr;    // peer-memory gather buffer (LL words, device.cuh XPeers)
   std::vector<void*> ipc_open;          // peer allocations mapped with cudaIpcOpenMemHandle
   std::vector<sx::XPeers> xpeers;       // per slab
@@ -170,7 +174,7 @@ struct simplex_s {
   }
   int kernels_per_segment() const {
     if (look == 1) return S * kernels_per_pivot();
-    if (gathered()) return steps_per_segment() * nslabs * (look + 2);   // k_mlook x (look+1), pass
+    if (gathered()) return steps_per_segment() * nslabs * (mblock ? 2 : look + 2);   // selection, pass
     return (look > sx::kMaxLook ? 3 : 2) * steps_per_segment();
   }
 
@@ -392,6 +396,22 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     NK(ncclCommInitRank(&comm, nranks, id, rank));
   }
   if (p2p) RET(setup_p2p());
+  if (p2p) {
+    // one k_mblock per part and block when every part's cluster can be resident at once (a rank
+    // per GPU; virtual slabs: nslabs clusters on this GPU, each on its own stream), else one
+    // k_mlook per pivot.  SIMPLEX_NO_MBLOCK=1: per-pivot launches (experiment hook)
+    const char* e = std::getenv("SIMPLEX_NO_MBLOCK");
+    mblock = !(e && e[0] == '1') && sx::mblock_max_clusters(slabs[0].look_grid, slabs[0].v.rows) >= nslabs;
+    if (mblock && nslabs > 1) {
+      xs.assign((size_t)nslabs, nullptr);
+      ev_join.assign((size_t)nslabs, nullptr);
+      for (int i = 0; i < nslabs; ++i) {
+        CK(cudaStreamCreateWithFlags(&xs[(size_t)i], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_join[(size_t)i], cudaEventDisableTiming));
+      }
+      CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    }
+  }
   return SIMPLEX_OK;
 }
 
@@ -530,6 +550,29 @@ simplex_err simplex_s::enqueue_pivot(int slot, int t) {
     // multi-part rank-s block: k_mlook for the block start and for every pivot on every part,
     // each followed by the exchange of the parts' candidate columns (exchange e in buffer e&1),
     // then the pass on every part's slab
+    if (mblock) {
+      // the block's selection: one k_mblock per part (virtual slabs concurrently, forked off the
+      // capture stream), then the pass on every slab
+      if (nslabs == 1) {
+        CK(sx::launch_mblock(slabs[0].v, nparts, xstride, look, opt.tol_opt, opt.tol_piv, slabs[0].look_grid,
+                             xpeers[0], stream));
+      } else {
+        CK(cudaEventRecord(ev_fork, stream));
+        for (int sidx = 0; sidx < nslabs; ++sidx) {
+          cudaStream_t q = xs[(size_t)sidx];
+          CK(cudaStreamWaitEvent(q, ev_fork, 0));
+          CK(sx::launch_mblock(slabs[sidx].v, nparts, xstride, look, opt.tol_opt, opt.tol_piv, slabs[sidx].look_grid,
+                               xpeers[(size_t)sidx], q));
+          CK(cudaEventRecord(ev_join[(size_t)sidx], q));
+          CK(cudaStreamWaitEvent(stream, ev_join[(size_t)sidx], 0));
+        }
+      }
+      if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
+      for (auto& sl : slabs)
+        CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
+      if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t + 1], stream, cudaEventRecordExternal));
+      return SIMPLEX_OK;
+    }
     double* X[2] = {recv, recv + (long long)nparts * xstride};
     static const sx::XPeers no_peers{};
     for (int u = -1; u < look; ++u) {
@@ -814,6 +857,11 @@ void simplex_s::release() {
   for (void* p : allocs) cudaFree(p);
   allocs.clear();
   if (h_state) cudaFreeHost(h_state);
+  for (auto q : xs)
+    if (q) cudaStreamDestroy(q);
+  for (auto e : ev_join)
+    if (e) cudaEventDestroy(e);
+  if (ev_fork) cudaEventDestroy(ev_fork);
   for (auto e : ev_done)
     if (e) cudaEventDestroy(e);
   if (ev_user) cudaEventDestroy(ev_user);

@@ -931,9 +931,9 @@ __device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned 
   return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
 }
 
-__global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double* __restrict__ xin,
-                                                       double* __restrict__ xout, int nparts, long long xstride,
-                                                       int t, int S, double tol_opt, double tol_piv, XPeers xp) {
+__device__ __forceinline__ void mlook_step(const SlabView& s, const double* __restrict__ xin,
+                                           double* __restrict__ xout, int nparts, long long xstride, int t, int S,
+                                           double tol_opt, double tol_piv, const XPeers& xp) {
   DevState* st = s.st;
   __shared__ int sh_r[kMaxLook];
   __shared__ __align__(16) Cand slot[2 * 16];
@@ -1097,6 +1097,27 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
     }
   }
   if (xp.n > 0 && gtid == 0) st->xseq = xseq + 1;
+}
+
+// One pivot t of a block per launch (t = -1: block start); the exchange between launches is
+// the NCCL allgather, plain stores (virtual slabs) or the peer-memory LL words.
+__global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double* __restrict__ xin,
+                                                       double* __restrict__ xout, int nparts, long long xstride,
+                                                       int t, int S, double tol_opt, double tol_piv, XPeers xp) {
+  mlook_step(s, xin, xout, nparts, xstride, t, S, tol_opt, tol_piv, xp);
+}
+
+// The whole block's selection in ONE launch per part (peer-memory exchange only): the steps
+// t = -1 .. S-1 of k_mlook back to back, each part polling the other parts' LL words of pivot t
+// inside the kernel — compute and exchange fused, no launch per pivot.  A cluster barrier between
+// steps publishes the step's DevState writes (status, it, xseq, rsb) to every CTA.  Every part
+// of the exchange must be resident at once (ranks: one per GPU; virtual slabs: one stream each).
+__global__ void __launch_bounds__(kLookThreads) k_mblock(SlabView s, int nparts, long long xstride, int S,
+                                                        double tol_opt, double tol_piv, XPeers xp) {
+  for (int t = -1; t < S; ++t) {
+    if (t >= 0) cluster_barrier();
+    mlook_step(s, nullptr, nullptr, nparts, xstride, t, S, tol_opt, tol_piv, xp);
+  }
 }
 
 // k_update_s: the rank-s pass, TMA in and TMA out.  CTA b owns column chunk c = b mod nc (cw
@@ -1507,6 +1528,26 @@ cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((s.rows + 31) / 32) * sizeof(unsigned int), st, attr);
   return cudaLaunchKernelEx(&cfg, k_mlook, s, xin, xout, nparts, xstride, t, S, tol_opt, tol_piv, xp);
+}
+
+cudaError_t launch_mblock(const SlabView& s, int nparts, long long xstride, int S, double tol_opt, double tol_piv,
+                          int cluster, const XPeers& xp, cudaStream_t st) {
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((s.rows + 31) / 32) * sizeof(unsigned int), st, attr);
+  return cudaLaunchKernelEx(&cfg, k_mblock, s, nparts, xstride, S, tol_opt, tol_piv, xp);
+}
+
+// Clusters of `cluster` CTAs of k_mblock that can be resident at once (0 on error).
+int mblock_max_clusters(int cluster, int rows) {
+  cudaFuncSetAttribute(k_mblock, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((rows + 31) / 32) * sizeof(unsigned int), nullptr, attr);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_mblock, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 // Shared memory of k_lookahead: the pivot-row bitmap, plus (nqc > 0) the previous bank's chain

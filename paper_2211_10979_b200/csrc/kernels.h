@@ -29,6 +29,10 @@ size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int*
 // xp.n > 0: the slot goes to every rank's gather buffer over peer memory + flags (no NCCL)
 cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int nparts, long long xstride, int t,
                          int S, double tol_opt, double tol_piv, int cluster, const XPeers& xp, cudaStream_t st);
+// k_mblock: the whole block's multi-part selection in one launch (peer-memory exchange only)
+cudaError_t launch_mblock(const SlabView& s, int nparts, long long xstride, int S, double tol_opt, double tol_piv,
+                          int cluster, const XPeers& xp, cudaStream_t st);
+int mblock_max_clusters(int cluster, int rows);
 int lookahead_cluster_size();
 int update_s_max(int S);
 int pass_cfg_choice(bool pipelined, double pass_bytes);   // k_update_s configuration (R rows x K stages)

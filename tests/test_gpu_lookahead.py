@@ -173,6 +173,16 @@ def test_multipart_klee_minty_and_ties(sx, P, xch):
         assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=8, exchange=xch), o)
 
 
+@pytest.mark.parametrize("P", [2, 5])
+def test_multipart_peer_exchange_per_pivot_launches(sx, P, monkeypatch):
+    """The peer-memory protocol with one k_mlook launch per pivot (SIMPLEX_NO_MBLOCK) instead of
+    one k_mblock per block (the virtual slabs then run in stream order, not concurrently)."""
+    monkeypatch.setenv("SIMPLEX_NO_MBLOCK", "1")
+    A, b, c = lpgen.dense_lp(120, 200, 77)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=16, exchange=2), o)
+
+
 def test_multipart_peer_exchange_reset_and_options(sx):
     """The exchange counters are monotone over the handle's life: a reset and a second solve
     reuse the flags; exchange = 2 (peer memory required) works on one GPU; bad values fail."""
