@@ -105,6 +105,8 @@ struct simplex_s {
   long long xstride = 0;
   bool p2p = false;                     // multi-part look-ahead exchanges over peer memory (no NCCL)
   bool mblock = false;                  // ... with the whole block's selection in one k_mblock launch
+  bool mpipe = false;                   // ... and that selection overlapped with the previous block's
+                                        //     slab passes (two tableau buffers per slab, §8)
   std::vector<cudaStream_t> xs;         // virtual slabs under k_mblock: one stream each (co-resident)
   cudaEvent_t ev_fork = nullptr;
   std::vector<cudaEvent_t> ev_join;
@@ -165,12 +167,12 @@ struct simplex_s {
   // brings the tableau back to buffer 0 at every segment boundary
   bool time_pass() const {                     // the pipelined pass is timed on the device
     static const bool time_sel = std::getenv("SIMPLEX_TIME_SELECT") != nullptr;
-    return opt.time_kernels && overlap && !time_sel;
+    return opt.time_kernels && (overlap || mpipe) && !time_sel;
   }
   int steps_per_segment() const {
     if (look == 1) return S;
     const int q = std::max(1, S / look);
-    return overlap ? (q + 1) / 2 * 2 : q;
+    return (overlap || mpipe) ? (q + 1) / 2 * 2 : q;
   }
   int kernels_per_segment() const {
     if (look == 1) return S * kernels_per_pivot();
@@ -195,6 +197,32 @@ struct simplex_s {
   simplex_err flush_all();
   void release();
   simplex_err setup_p2p();
+  // the multi-part selection of one block: one k_mblock per slab (forked onto the selection
+  // streams when there are several slabs or the passes run concurrently); join = false leaves the
+  // join to the caller (after the concurrent passes)
+  simplex_err mselect(int q, int bown, int bpre, bool join) {
+    if (xs.empty()) {
+      const Slab& sl = slabs[0];
+      CK(sx::launch_mblock(sl.v, q ? sl.T2 : sl.v.T, nparts, xstride, look, bown, bpre, opt.tol_opt, opt.tol_piv,
+                           sl.look_grid, xpeers[0], stream));
+      return SIMPLEX_OK;
+    }
+    CK(cudaEventRecord(ev_fork, stream));
+    for (int sidx = 0; sidx < nslabs; ++sidx) {
+      const Slab& sl = slabs[sidx];
+      cudaStream_t x = xs[(size_t)sidx];
+      CK(cudaStreamWaitEvent(x, ev_fork, 0));
+      CK(sx::launch_mblock(sl.v, q ? sl.T2 : sl.v.T, nparts, xstride, look, bown, bpre, opt.tol_opt, opt.tol_piv,
+                           sl.look_grid, xpeers[(size_t)sidx], x));
+      CK(cudaEventRecord(ev_join[(size_t)sidx], x));
+    }
+    if (join) RET(mjoin());
+    return SIMPLEX_OK;
+  }
+  simplex_err mjoin() {
+    for (auto e : ev_join) CK(cudaStreamWaitEvent(stream, e, 0));
+    return SIMPLEX_OK;
+  }
 };
 
 // Rows with b_i < 0 (1-based, ascending) and their artificial index (reading p1).
@@ -306,6 +334,19 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     if (look > 1) {
       sl.look_grid = sx::lookahead_cluster_size();
       if (sl.look_grid < 1) return fail(SIMPLEX_E_CUDA, "look-ahead selection cluster cannot be scheduled");
+      if (s == 0 && p2p) {
+        // one k_mblock per part and block when every part's cluster can be resident at once (a
+        // rank per GPU; virtual slabs: nslabs clusters on this GPU, each on its own stream), else
+        // one k_mlook per pivot (also SIMPLEX_NO_MBLOCK=1, experiment hook); pipelined with the
+        // slab passes (overlap = 1) when two tableau buffers per slab fit
+        const char* e = std::getenv("SIMPLEX_NO_MBLOCK");
+        mblock = !(e && e[0] == '1') && sx::mblock_max_clusters(sl.look_grid, v.rows) >= nslabs;
+        if (mblock && opt.overlap != 0) {
+          size_t free_b = 0, total_b = 0;
+          CK(cudaMemGetInfo(&free_b, &total_b));
+          mpipe = 2.2 * 8.0 * (double)v.rows * (double)v.ld * nslabs <= (double)free_b;
+        }
+      }
       // k_update_s: column chunks of cw doubles x row groups; all CTAs resident
       // (nc, cw, Gr) minimising the busiest CTA's share cw * ceil(rows / Gr) over the
       // occ * sms resident slots (pipelined: the SMs left over by the selection cluster),
@@ -313,11 +354,12 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       // 296 CTAs at 8000^2 instead of 32 x 9 = 288)
       const int cwmax = 2 * sx::kThreads;
       int occ = 1;
-      pass_cfg = sx::pass_cfg_choice(overlap, 16.0 * v.rows * v.ld);   // bytes read + written per pass
+      pass_cfg = sx::pass_cfg_choice(overlap || mpipe, 16.0 * v.rows * v.ld);   // bytes read + written per pass
       CK(sx::update_s_occupancy(pass_cfg, look, &occ, sx::update_s_smem(pass_cfg, cwmax, v.rows, look)));
       if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
       const char* ps = getenv("SIMPLEX_PASS_SMS");          // experiment hook
-      const long long slots = (long long)occ * (ps ? atoi(ps) : overlap ? sms - sl.look_grid : sms);
+      const long long slots = (long long)occ * (ps ? atoi(ps) : overlap ? sms - sl.look_grid
+                                                                : mpipe ? sms - nslabs * sl.look_grid : sms);
       const long long nc0 = (v.ld + cwmax - 1) / cwmax;
       long long best = LLONG_MAX;
       for (long long nc = nc0; nc <= std::max(nc0, std::min(slots, 4 * nc0)); ++nc) {
@@ -349,7 +391,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     RET(dalloc(&v.price, v.nslot));
     RET(dalloc(&v.col, v.rows + 2));
     RET(dalloc(&v.rownorm, v.ld));
-    if (overlap) RET(dalloc(&sl.T2, (size_t)v.rows * v.ld));
+    if (overlap || mpipe) RET(dalloc(&sl.T2, (size_t)v.rows * v.ld));
     RET(dalloc(&v.rcand, std::max(sl.sel_grid, sl.look_grid)));
     RET(dalloc(&v.basis, m));
     RET(dalloc(&v.art_of_row, m));
@@ -396,21 +438,15 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     NK(ncclCommInitRank(&comm, nranks, id, rank));
   }
   if (p2p) RET(setup_p2p());
-  if (p2p) {
-    // one k_mblock per part and block when every part's cluster can be resident at once (a rank
-    // per GPU; virtual slabs: nslabs clusters on this GPU, each on its own stream), else one
-    // k_mlook per pivot.  SIMPLEX_NO_MBLOCK=1: per-pivot launches (experiment hook)
-    const char* e = std::getenv("SIMPLEX_NO_MBLOCK");
-    mblock = !(e && e[0] == '1') && sx::mblock_max_clusters(slabs[0].look_grid, slabs[0].v.rows) >= nslabs;
-    if (mblock && nslabs > 1) {
-      xs.assign((size_t)nslabs, nullptr);
-      ev_join.assign((size_t)nslabs, nullptr);
-      for (int i = 0; i < nslabs; ++i) {
-        CK(cudaStreamCreateWithFlags(&xs[(size_t)i], cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&ev_join[(size_t)i], cudaEventDisableTiming));
-      }
-      CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  if (!p2p) mblock = mpipe = false;              // peers unreachable: NCCL per pivot
+  if (mblock && nslabs > 1) {                     // selection streams (forked inside the graphs)
+    xs.assign((size_t)nslabs, nullptr);
+    ev_join.assign((size_t)nslabs, nullptr);
+    for (int i = 0; i < nslabs; ++i) {
+      CK(cudaStreamCreateWithFlags(&xs[(size_t)i], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev_join[(size_t)i], cudaEventDisableTiming));
     }
+    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
   }
   return SIMPLEX_OK;
 }
@@ -550,23 +586,30 @@ simplex_err simplex_s::enqueue_pivot(int slot, int t) {
     // multi-part rank-s block: k_mlook for the block start and for every pivot on every part,
     // each followed by the exchange of the parts' candidate columns (exchange e in buffer e&1),
     // then the pass on every part's slab
-    if (mblock) {
-      // the block's selection: one k_mblock per part (virtual slabs concurrently, forked off the
-      // capture stream), then the pass on every slab
-      if (nslabs == 1) {
-        CK(sx::launch_mblock(slabs[0].v, nparts, xstride, look, opt.tol_opt, opt.tol_piv, slabs[0].look_grid,
-                             xpeers[0], stream));
-      } else {
-        CK(cudaEventRecord(ev_fork, stream));
-        for (int sidx = 0; sidx < nslabs; ++sidx) {
-          cudaStream_t q = xs[(size_t)sidx];
-          CK(cudaStreamWaitEvent(q, ev_fork, 0));
-          CK(sx::launch_mblock(slabs[sidx].v, nparts, xstride, look, opt.tol_opt, opt.tol_piv, slabs[sidx].look_grid,
-                               xpeers[(size_t)sidx], q));
-          CK(cudaEventRecord(ev_join[(size_t)sidx], q));
-          CK(cudaStreamWaitEvent(stream, ev_join[(size_t)sidx], 0));
-        }
+    if (mpipe) {
+      // multi-part pipeline (the §9e scheme on P parts): block t's starting tableau is in buffer
+      // t&1 of every slab and its pivots in bank t&1; select block t+1 (chaining block t first)
+      // on the selection streams WHILE block t's slab passes (buffer t&1 -> the other) run here
+      // One stream, programmatic dependent launch (as in §9e): the first part's selection is a
+      // normal launch (everything before it has finished), the other parts' selections and then
+      // the slab passes are launched behind it without waiting, so every selection cluster is
+      // placed before the passes fill the remaining SMs.  The pass times itself on the device
+      // (time_kernels) because event nodes would serialize it after the selections.
+      const int q = t & 1;
+      for (int sidx = 0; sidx < nslabs; ++sidx) {
+        const Slab& sl = slabs[sidx];
+        CK(sx::launch_mblock(sl.v, q ? sl.T2 : sl.v.T, nparts, xstride, look, q ^ 1, q, opt.tol_opt, opt.tol_piv,
+                             sl.look_grid, xpeers[(size_t)sidx], stream, sidx > 0));
       }
+      for (auto& sl : slabs) {
+        double* buf[2] = {sl.v.T, sl.T2};
+        CK(sx::launch_update_s(pass_cfg, sl.v, look, buf[q], buf[q ^ 1], q, sl.nc, sl.Gr, sl.cw, stream, true));
+      }
+      return SIMPLEX_OK;
+    }
+    if (mblock) {
+      // the block's selection: one k_mblock per part (virtual slabs concurrently), then the passes
+      RET(mselect(0, 0, -1, true));
       if (opt.time_kernels) CK(cudaEventRecordWithFlags(tev[slot][2 * t], stream, cudaEventRecordExternal));
       for (auto& sl : slabs)
         CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
@@ -717,6 +760,10 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
       CK(sx::launch_lookahead(sl.v, sl.v.T, look, 0, -1, opt.tol_opt, opt.tol_piv, sl.look_grid, false, stream));
       ++kernel_launches;
     }
+    if (mpipe) {                                  // multi-part pipeline prologue (bank 0, buffer 0)
+      RET(mselect(0, 0, -1, true));
+      kernel_launches += nslabs;
+    }
     long long launched = 0, completed = 0, seen = it;
     bool stop = false;
     for (;;) {
@@ -762,6 +809,11 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
       const Slab& sl = slabs[0];
       CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
       ++kernel_launches;
+    }
+    if (mpipe) {                                  // multi-part pipeline drain
+      for (auto& sl : slabs)
+        CK(sx::launch_update_s(pass_cfg, sl.v, look, sl.v.T, sl.v.T, 0, sl.nc, sl.Gr, sl.cw, stream, false));
+      kernel_launches += nslabs;
     }
     // Phase I optimal: decide feasibility, drive artificials out, install the objective
     if (status == SIMPLEX_OPTIMAL && phase == 1) {

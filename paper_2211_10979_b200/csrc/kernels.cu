@@ -931,11 +931,17 @@ __device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned 
   return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
 }
 
-__device__ __forceinline__ void mlook_step(const SlabView& s, const double* __restrict__ xin,
-                                           double* __restrict__ xout, int nparts, long long xstride, int t, int S,
-                                           double tol_opt, double tol_piv, const XPeers& xp) {
+// One step of the multi-part selection (see k_mlook / k_mblock).  T: the tableau the chains
+// start from; own pivots go to chain bank `bown`.  bpre >= 0 (multi-part pipeline): T is the
+// tableau BEFORE the previous block, whose pass runs concurrently; its pivots (bank bpre) are
+// chained first and R0 / RHS continue from the previous block (the §9e scheme on P parts).
+__device__ __forceinline__ void mlook_step(const SlabView& s, const double* __restrict__ T,
+                                           const double* __restrict__ xin, double* __restrict__ xout, int nparts,
+                                           long long xstride, int t, int S, int bown, int bpre, double tol_opt,
+                                           double tol_piv, const XPeers& xp) {
   DevState* st = s.st;
-  __shared__ int sh_r[kMaxLook];
+  __shared__ int sh_r[kMaxLook];                      // own pivot rows
+  __shared__ int sh_rp[kMaxLook];                     // pivot rows of the previous bank
   __shared__ __align__(16) Cand slot[2 * 16];
   extern __shared__ unsigned int piv_mark[];
   const long long gthreads = (long long)gridDim.x * blockDim.x;
@@ -944,15 +950,17 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
   const long long ld = s.ld;
   const int w = s.w;
   const int pw = st->pw;
-  double* __restrict__ colS = s.colS;                 // bank 0, row stride kColS
-  double* __restrict__ prowS = s.prowS;               // bank 0, rows u = 0..15
+  double* __restrict__ colO = s.colS + bown * kMaxLook;                 // row stride kColS
+  double* __restrict__ prowO = s.prowS + (long long)bown * kMaxLook * ld;
+  const double* __restrict__ colP = s.colS + (bpre >= 0 ? bpre : 0) * kMaxLook;
+  const double* __restrict__ prowP = s.prowS + (long long)(bpre >= 0 ? bpre : 0) * kMaxLook * ld;
   double* __restrict__ R0 = s.R0;
   double* __restrict__ RHS = s.RHS;
-  const double* __restrict__ T = s.T;
   long long it = st->it;
-  if (t < 0 && gtid == 0) st->sb[0] = 0;             // the block is empty until a pivot is taken
+  if (t < 0 && gtid == 0) st->sb[bown] = 0;          // the block is empty until a pivot is taken
   const bool active = st->status == kRunning && it < st->stop_at;
   if (!active) return;                                // uniform: every CTA reads the same state
+  const int spre = bpre >= 0 ? st->sb[bpre] : 0;
   // peer-memory exchange: the slots of this pivot carry sequence number xseq (every part has
   // published as many slots as this one); this launch publishes xseq + 1
   const unsigned int xseq = xp.n > 0 ? (unsigned int)st->xseq : 0u;
@@ -961,21 +969,34 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
   auto xget = [&](int q, long long e) -> double {
     return xll ? ll_load(xll + 2 * ((long long)q * xstride + e), xseq, st) : __ldcg(xin + (long long)q * xstride + e);
   };
+  // pivot-row bitmap of both banks (own pivots 0..t-1)
+  for (int q = threadIdx.x; q < (rows + 31) / 32; q += blockDim.x) piv_mark[q] = 0u;
+  if ((int)threadIdx.x < kMaxLook) {
+    sh_rp[threadIdx.x] = (int)threadIdx.x < spre ? st->rsb[bpre][threadIdx.x] : -1;
+    sh_r[threadIdx.x] = (int)threadIdx.x < t ? st->rsb[bown][threadIdx.x] : -1;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < spre) atomicOr(&piv_mark[sh_rp[threadIdx.x] >> 5], 1u << (sh_rp[threadIdx.x] & 31));
+  if ((int)threadIdx.x < t) atomicOr(&piv_mark[sh_r[threadIdx.x] >> 5], 1u << (sh_r[threadIdx.x] & 31));
+  __syncthreads();
   int ph = 0;
   Cand best = cand_none();
   int r = -1;                                         // pivot row of step t (t >= 0)
   if (t < 0) {
-    for (long long j = gtid; j < ld; j += gthreads) {
-      const double v = T[j];
-      R0[j] = v;
-      if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+    if (bpre < 0) {
+      for (long long j = gtid; j < ld; j += gthreads) {
+        const double v = T[j];
+        R0[j] = v;
+        if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+      }
+      for (long long i = gtid; i < rows; i += gthreads) RHS[i] = T[i * ld + w];
+    } else {                                          // R0 continues from the previous block
+      for (long long j = gtid; j < pw; j += gthreads) {
+        const double v = R0[j];
+        if (v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+      }
     }
-    for (long long i = gtid; i < rows; i += gthreads) RHS[i] = T[i * ld + w];
   } else {
-    for (int q = threadIdx.x; q < (rows + 31) / 32; q += blockDim.x) piv_mark[q] = 0u;
-    if ((int)threadIdx.x < t) sh_r[threadIdx.x] = st->rsb[0][threadIdx.x];
-    __syncthreads();
-    if ((int)threadIdx.x < t) atomicOr(&piv_mark[sh_r[threadIdx.x] >> 5], 1u << (sh_r[threadIdx.x] & 31));
     // Step 1: fold the gathered candidates (every part the same)
     Cand kb = cand_none();
     int q = -1;
@@ -988,16 +1009,19 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
       return;
     }
     const long long k = kb.idx;
-    // Step 2 over all rows; the rhs gets pivot t-1 first
-    const int r_prev = t > 0 ? st->rsb[0][t - 1] : -1;
-    const double pw_prev = t > 0 ? __ldcg(prowS + (long long)(t - 1) * ld + w) : 0.0;
+    // Step 2 over all rows; the rhs gets the previous pivot first (at t = 0 of a pipelined
+    // block: the previous block's last pivot)
+    const int r_prev = t > 0 ? st->rsb[bown][t - 1] : spre > 0 ? sh_rp[spre - 1] : -1;
+    const double* c_prev = t > 0 ? colO + t - 1 : colP + (spre > 0 ? spre - 1 : 0);
+    const double pw_prev = r_prev < 0 ? 0.0
+                           : __ldcg((t > 0 ? prowO + (long long)(t - 1) * ld : prowP + (long long)(spre - 1) * ld) + w);
     Cand rb = cand_none();
     for (long long i = gtid; i < rows; i += gthreads) {
       double h = RHS[i];
-      if (t > 0) h = (i == r_prev) ? pw_prev : __fma_rn(-colS[i * kColS + t - 1], pw_prev, h);
+      if (r_prev >= 0) h = (i == r_prev) ? pw_prev : __fma_rn(-c_prev[i * kColS], pw_prev, h);
       RHS[i] = h;
       const double x = xget(q, 2 + i);
-      colS[i * kColS + t] = x;
+      colO[i * kColS + t] = x;
       if (i >= 1 && x > tol_piv) {
         int basic = 0;
         if (s.rule) basic = __ldcg(s.basis + i - 1);
@@ -1020,20 +1044,29 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
     r = cand_row(rb.idx);
     const double p = xget(q, 2 + r);
     const double a0 = -xget(q, 2);
-    double cr[kMaxLook];
+    double cr[kMaxLook], cs[kMaxLook];
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? __ldcg(colS + (long long)r * kColS + u) : 0.0;
-    unsigned int rmask = 0u;
+    for (int u = 0; u < kMaxLook; ++u) cs[u] = u < spre ? __ldcg(colP + (long long)r * kColS + u) : 0.0;
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u)
+    for (int u = 0; u < kMaxLook; ++u) cr[u] = u < t ? __ldcg(colO + (long long)r * kColS + u) : 0.0;
+    unsigned int rmask = 0u, qmask = 0u;
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) {
       if (u < t && sh_r[u] == r) rmask |= 1u << u;
+      if (u < spre && sh_rp[u] == r) qmask |= 1u << u;
+    }
     const double* Tr = T + (long long)r * ld;
-    double* prow = prowS + (long long)t * ld;
+    double* prow = prowO + (long long)t * ld;
     for (long long j = gtid; j < ld; j += gthreads) {
       double x = Tr[j];
-      double pu[kMaxLook];
+      double qu[kMaxLook], pu[kMaxLook];
 #pragma unroll
-      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? prowS[(long long)u * ld + j] : 0.0;
+      for (int u = 0; u < kMaxLook; ++u) qu[u] = u < spre ? prowP[(long long)u * ld + j] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u) pu[u] = u < t ? prowO[(long long)u * ld + j] : 0.0;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u)
+        if (u < spre) x = ((qmask >> u) & 1u) ? qu[u] : __fma_rn(-cs[u], qu[u], x);
 #pragma unroll
       for (int u = 0; u < kMaxLook; ++u)
         if (u < t) x = ((rmask >> u) & 1u) ? pu[u] : __fma_rn(-cr[u], pu[u], x);
@@ -1044,8 +1077,8 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
       if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
     }
     if (gtid == 0) {
-      st->rsb[0][t] = r;
-      st->sb[0] = t + 1;
+      st->rsb[bown][t] = r;
+      st->sb[bown] = t + 1;
       s.basis[r - 1] = (int)k;
       if (it < s.trace_cap) {
         s.trace_k[it] = (int)k;
@@ -1075,17 +1108,26 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
   }
   if (best.idx != LLONG_MAX) {
     const long long kc = best.idx - s.c0;
-    const int nu = t + 1;                             // chains applied: pivots 0..t
-    double pk[kMaxLook];
+    const int nu = t + 1;                             // own chains applied: pivots 0..t
+    double qk[kMaxLook], pk[kMaxLook];
 #pragma unroll
-    for (int u = 0; u < kMaxLook; ++u) pk[u] = u < nu ? __ldcg(prowS + (long long)u * ld + kc) : 0.0;
+    for (int u = 0; u < kMaxLook; ++u) qk[u] = u < spre ? __ldcg(prowP + (long long)u * ld + kc) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) pk[u] = u < nu ? __ldcg(prowO + (long long)u * ld + kc) : 0.0;
     for (long long i = gtid; i < rows; i += gthreads) {
       double x = T[i * ld + kc];
-      const bool marked = (t >= 0) && ((piv_mark[i >> 5] >> (i & 31)) & 1u);
+      const bool marked = (piv_mark[i >> 5] >> (i & 31)) & 1u;
+#pragma unroll
+      for (int u = 0; u < kMaxLook; ++u) {
+        if (u < spre) {
+          const double cq = colP[i * kColS + u];
+          x = (marked && i == sh_rp[u]) ? qk[u] : __fma_rn(-cq, qk[u], x);
+        }
+      }
 #pragma unroll
       for (int u = 0; u < kMaxLook; ++u) {
         if (u < nu) {
-          const double cu = colS[i * kColS + u];
+          const double cu = colO[i * kColS + u];
           x = (marked && i == sh_r[u]) ? pk[u] : __fma_rn(-cu, pk[u], x);
         }
       }
@@ -1104,7 +1146,7 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
 __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double* __restrict__ xin,
                                                        double* __restrict__ xout, int nparts, long long xstride,
                                                        int t, int S, double tol_opt, double tol_piv, XPeers xp) {
-  mlook_step(s, xin, xout, nparts, xstride, t, S, tol_opt, tol_piv, xp);
+  mlook_step(s, s.T, xin, xout, nparts, xstride, t, S, 0, -1, tol_opt, tol_piv, xp);
 }
 
 // The whole block's selection in ONE launch per part (peer-memory exchange only): the steps
@@ -1112,11 +1154,14 @@ __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double
 // inside the kernel — compute and exchange fused, no launch per pivot.  A cluster barrier between
 // steps publishes the step's DevState writes (status, it, xseq, rsb) to every CTA.  Every part
 // of the exchange must be resident at once (ranks: one per GPU; virtual slabs: one stream each).
-__global__ void __launch_bounds__(kLookThreads) k_mblock(SlabView s, int nparts, long long xstride, int S,
-                                                        double tol_opt, double tol_piv, XPeers xp) {
+__global__ void __launch_bounds__(kLookThreads) k_mblock(SlabView s, const double* __restrict__ T, int nparts,
+                                                        long long xstride, int S, int bown, int bpre, double tol_opt,
+                                                        double tol_piv, XPeers xp) {
+  pdl_launch_dependents();            // (multi-part pipeline: the next part's selection and the slab
+                                      //  passes are launched behind this one without waiting)
   for (int t = -1; t < S; ++t) {
     if (t >= 0) cluster_barrier();
-    mlook_step(s, nullptr, nullptr, nparts, xstride, t, S, tol_opt, tol_piv, xp);
+    mlook_step(s, T, nullptr, nullptr, nparts, xstride, t, S, bown, bpre, tol_opt, tol_piv, xp);
   }
 }
 
@@ -1530,11 +1575,17 @@ cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int
   return cudaLaunchKernelEx(&cfg, k_mlook, s, xin, xout, nparts, xstride, t, S, tol_opt, tol_piv, xp);
 }
 
-cudaError_t launch_mblock(const SlabView& s, int nparts, long long xstride, int S, double tol_opt, double tol_piv,
-                          int cluster, const XPeers& xp, cudaStream_t st) {
-  cudaLaunchAttribute attr[1];
+cudaError_t launch_mblock(const SlabView& s, const double* T, int nparts, long long xstride, int S, int bown,
+                          int bpre, double tol_opt, double tol_piv, int cluster, const XPeers& xp, cudaStream_t st,
+                          bool pdl) {
+  cudaLaunchAttribute attr[2];
   cudaLaunchConfig_t cfg = lookahead_config(cluster, (size_t)((s.rows + 31) / 32) * sizeof(unsigned int), st, attr);
-  return cudaLaunchKernelEx(&cfg, k_mblock, s, nparts, xstride, S, tol_opt, tol_piv, xp);
+  if (pdl) {
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
+  return cudaLaunchKernelEx(&cfg, k_mblock, s, T, nparts, xstride, S, bown, bpre, tol_opt, tol_piv, xp);
 }
 
 // Clusters of `cluster` CTAs of k_mblock that can be resident at once (0 on error).

@@ -30,8 +30,10 @@ size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int*
 cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int nparts, long long xstride, int t,
                          int S, double tol_opt, double tol_piv, int cluster, const XPeers& xp, cudaStream_t st);
 // k_mblock: the whole block's multi-part selection in one launch (peer-memory exchange only)
-cudaError_t launch_mblock(const SlabView& s, int nparts, long long xstride, int S, double tol_opt, double tol_piv,
-                          int cluster, const XPeers& xp, cudaStream_t st);
+// (T: the tableau the chains start from; bpre >= 0: the previous block's bank is chained first)
+cudaError_t launch_mblock(const SlabView& s, const double* T, int nparts, long long xstride, int S, int bown,
+                          int bpre, double tol_opt, double tol_piv, int cluster, const XPeers& xp, cudaStream_t st,
+                          bool pdl = false);
 int mblock_max_clusters(int cluster, int rows);
 int lookahead_cluster_size();
 int update_s_max(int S);

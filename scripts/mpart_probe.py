@@ -37,6 +37,8 @@ if os.environ.get("SIMPLEX_FORCE_NCCL"):
     sys.exit(0)
 timed("1 part, pipelined")
 for P in (2, 4):
-    timed(f"{P} virtual slabs look16, peer-memory protocol", virtual_ranks=P, exchange=2)
+    timed(f"{P} virtual slabs look16, peer-memory protocol, pipelined", virtual_ranks=P, exchange=2)
+    timed(f"{P} virtual slabs look16, peer-memory protocol, select then pass", virtual_ranks=P, exchange=2,
+          overlap=False)
     timed(f"{P} virtual slabs look16, direct (stream order)", virtual_ranks=P)
     timed(f"{P} virtual slabs one pivot per pass", virtual_ranks=P, lookahead=1)

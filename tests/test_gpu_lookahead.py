@@ -173,6 +173,17 @@ def test_multipart_klee_minty_and_ties(sx, P, xch):
         assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=8, exchange=xch), o)
 
 
+@pytest.mark.parametrize("look", [5, 16])
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_multipart_peer_exchange_without_pipeline(sx, P, look):
+    """k_mblock per block, select-then-pass (overlap = 0); the default (overlap = 1) selects block
+    b+1 from the tableau before block b's slab passes while they run, on two buffers per slab."""
+    A, b, c = lpgen.dense_lp(150, 170, 9)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=look, exchange=2, overlap=False), o)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=look, exchange=2, overlap=True), o)
+
+
 @pytest.mark.parametrize("P", [2, 5])
 def test_multipart_peer_exchange_per_pivot_launches(sx, P, monkeypatch):
     """The peer-memory protocol with one k_mlook launch per pivot (SIMPLEX_NO_MBLOCK) instead of
