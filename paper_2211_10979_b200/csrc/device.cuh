@@ -108,6 +108,8 @@ struct SlabView {
   // Two banks of chains: bank q holds pivots u = 0..15 at colS[i][16q+u], prowS[16q+u][.]
   double* colS;        // [rows][kColS]     pivot columns T^t[.][k_t], t-minor
   double* prowS;       // [kColS][ld]       normalized pivot rows T^t[r_t][.] / p_t
+  double* colT;        // [2][16][rows]     the same pivot columns, transposed (bank, t, row): the
+                       //                   selection's per-row chain loads coalesce across a warp
   double* R0;          // [ld]              current objective row during selection
   double* RHS;         // [rows]            current rhs column during selection
   Cand* pcand;         // [look-ahead CTAs] Step-1 candidates per CTA

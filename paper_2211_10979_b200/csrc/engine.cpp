@@ -405,6 +405,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     if (look > 1) {
       RET(dalloc(&v.colS, (size_t)v.rows * sx::kColS));
       RET(dalloc(&v.prowS, (size_t)sx::kColS * v.ld));
+      RET(dalloc(&v.colT, (size_t)v.rows * sx::kColS));
       RET(dalloc(&v.R0, v.ld));
       RET(dalloc(&v.RHS, v.rows));
       RET(dalloc(&v.pcand, sl.look_grid));

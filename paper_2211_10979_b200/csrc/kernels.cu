@@ -647,6 +647,9 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   const int pw = st->pw;                              // priced columns (Phase II: no artificials)
   double* __restrict__ colO = s.colS + bown * kMaxLook;                 // row stride kColS
   const double* __restrict__ colP = s.colS + (bpre >= 0 ? bpre : 0) * kMaxLook;
+  // transposed copies [t][row] of both banks: per-row loads of a warp hit consecutive rows
+  double* __restrict__ colTo = s.colT + (size_t)bown * kMaxLook * rows;
+  const double* __restrict__ colTp = s.colT + (size_t)(bpre >= 0 ? bpre : 0) * kMaxLook * rows;
   double* __restrict__ prowO = s.prowS + (long long)bown * kMaxLook * ld;
   const double* __restrict__ prowP = s.prowS + (long long)(bpre >= 0 ? bpre : 0) * kMaxLook * ld;
   double* __restrict__ R0 = s.R0;
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
           if (u < spre)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                              smem_u32(&cR[((size_t)u * nqr + q) * blockDim.x + threadIdx.x])),
-                         "l"(colP + i * kColS + u)
+                         "l"(colTp + (size_t)u * rows + i)
                          : "memory");
       }
     }
@@ -729,7 +732,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
   if (cache) asm volatile("cp.async.wait_group 0;" ::: "memory");   // own entries only: no barrier
   int t = 0;
   int r_prev = spre > 0 ? sh_rp[spre - 1] : -1;       // pivot not yet applied to RHS
-  const double* c_prev = spre > 0 ? colP + spre - 1 : nullptr;
+  const double* c_prev = spre > 0 ? colTp + (size_t)(spre - 1) * rows : nullptr;   // transposed
   const double* p_prev = spre > 0 ? prowP + (long long)(spre - 1) * ld : nullptr;
   for (; t < S; ++t) {
     if (status != kRunning || it >= stop) break;
@@ -753,9 +756,9 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
         const bool v = b == 0 || i < rows;
         xb[b] = v ? T[i * ld + k] : 0.0;
         hb[b] = v ? RHS[i] : 0.0;
-        cpb[b] = v && r_prev >= 0 ? c_prev[i * kColS] : 0.0;
+        cpb[b] = v && r_prev >= 0 ? c_prev[i] : 0.0;
 #pragma unroll
-        for (int u = 0; u < kMaxLook; ++u) cub[b][u] = v && u < t ? colO[i * kColS + u] : 0.0;
+        for (int u = 0; u < kMaxLook; ++u) cub[b][u] = v && u < t ? colTo[(size_t)u * rows + i] : 0.0;
       }
 #pragma unroll
       for (int b = 0; b < kLookRB; ++b) {
@@ -767,7 +770,8 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
         double cq[kMaxLook];                              // this row's previous-bank column entries
 #pragma unroll
         for (int u = 0; u < kMaxLook; ++u)
-          cq[u] = u < spre ? (cache ? cR[((size_t)u * nqr + qi) * blockDim.x + threadIdx.x] : colP[i * kColS + u]) : 0.0;
+          cq[u] = u < spre ? (cache ? cR[((size_t)u * nqr + qi) * blockDim.x + threadIdx.x] : colTp[(size_t)u * rows + i])
+                           : 0.0;
         if (r_prev >= 0) h = (i == r_prev) ? pw_prev : __fma_rn(-cpb[b], pw_prev, h);
         RHS[i] = h;
         if ((piv_mark[i >> 5] >> (i & 31)) & 1u) {       // row i is a pivot row of a pending chain
@@ -785,7 +789,8 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
           for (int u = 0; u < kMaxLook; ++u)
             if (u < t) x = __fma_rn(-cub[b][u], pk[u], x);
         }
-        colO[i * kColS + t] = x;
+        colO[i * kColS + t] = x;                       // (row-major: the pass's TMA rows)
+        colTo[(size_t)t * rows + i] = x;
         if (i >= 1 && x > tol_piv)                                              // Step 2
           rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
       }
@@ -868,7 +873,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     }
     ++it;
     r_prev = r;
-    c_prev = colO + t;
+    c_prev = colTo + (size_t)t * rows;
     p_prev = prow;
     SX_PROBE(4 + 4 * t);
     best = cluster_min(best, slot, ph);
