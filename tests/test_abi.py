@@ -105,6 +105,16 @@ def test_argument_errors_before_any_device_work():
     bad.struct_size = 7
     assert sx.lib().simplex_create(C.byref(h), 2, 2, A.ctypes.data, b.ctypes.data, c.ctypes.data,
                                    C.byref(bad)) == sx.E_ARG
+    # option values rejected before any device work: exchange outside 0..2, lookahead > 32, the
+    # pair schedule (lookahead 17..32) on several column parts
+    for field, value, extra in (("exchange", 3, {}), ("exchange", -1, {}), ("lookahead", 33, {}),
+                                ("lookahead", 32, {"virtual_ranks": 2})):
+        o = sx.default_options()
+        setattr(o, field, value)
+        for k, v in extra.items():
+            setattr(o, k, v)
+        assert sx.lib().simplex_create(C.byref(h), 2, 2, A.ctypes.data, b.ctypes.data, c.ctypes.data,
+                                       C.byref(o)) == sx.E_ARG, (field, value, extra)
 
 
 def test_no_cpu_fallback_without_gpu():
