@@ -229,6 +229,27 @@ def test_nccl_exchange_path_one_rank(sx, monkeypatch):
     assert_same(g, o)
 
 
+def test_wide_prefix_20000x40000_pipelined_512(sx):
+    """BASELINE config 5 in the launch configuration bench.py times (library default: rank-16
+    look-ahead, selection pipelined with the pass, two 9.6 GB tableau buffers): 32 blocks, the
+    first 512 pivots, against the oracle's 512-pivot prefix run (tests/golden/*_p512.npz)."""
+    g = np.load(os.path.join(GOLDEN_DIR, "dense_20000x40000_s1_p512.npz"))
+    A, b, c = lpgen.dense_lp(20000, 40000, 1)
+    with sx.Simplex(A, b, c) as s:
+        done, st = s.iterate(512)
+        assert done == 512 and st == sx.RUNNING
+        k, r = s.trace()
+        h = s.tableau_hash()
+        x, y, obj, piv, _ = s.solution()
+    assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+    assert obj == float(g["objective"])
+    assert np.array_equal(y, g["y"])
+    xs = np.zeros(40000)
+    xs[g["x_idx"]] = g["x_val"]
+    assert np.array_equal(x, xs)
+    assert h == int(g["tableau_hash"])
+
+
 def test_wide_prefix_20000x40000(sx):
     """BASELINE config 5 (~9.6 GB tableau): the first 32 pivots, row 0, rhs column and the
     whole-tableau digest against the oracle's prefix run (tests/golden/*_p32.npz)."""
