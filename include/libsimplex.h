@@ -105,8 +105,9 @@ typedef struct {
                                with T[0][j] < -tol_opt, ratio ties -> smallest basic-variable
                                index (anti-cycling)   */
     int32_t  phase1;        /* 1 (default): b with negative entries runs the two-phase method
-                               (artificials, Phase I objective, drive-out, Phase II; one
-                               column part) and may end INFEASIBLE;
+                               (artificials, Phase I objective, drive-out, Phase II; every
+                               path incl. column parts) and may end
+                               INFEASIBLE;
                                0: b_i < 0 is rejected with SIMPLEX_E_NEG_RHS               */
     int32_t  overlap;       /* rank-s look-ahead only.  1 (default): software pipeline —
                                block b+1 is selected (on one thread-block cluster) WHILE

@@ -119,6 +119,8 @@ struct simplex_s {
   double* d_obj = nullptr;
   double* d_b = nullptr;
   unsigned long long* d_hash = nullptr;
+  double* d_fcol = nullptr;             // Phase I drive-out on several parts: the pivot column
+  long long* d_fj = nullptr;            // ... and its global index (allreduced across ranks)
   sx::DevState* h_state = nullptr;  // pinned, 3 slots: 2 segment mirrors + 1 sync copy
   // graph segments
   int S = 32;                       // pivots per captured graph segment
@@ -295,9 +297,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   RET(scan_b(b, &art_of_row, &art_rows));
   arts = (long long)art_rows.size();
   W = n + m + arts + 1;
-  if (arts > 0 && (nparts > 1 || !opt.phase1))
-    return fail(SIMPLEX_E_NEG_RHS, nparts > 1 ? "b has negative entries: Phase I runs on one column part only"
-                                              : "b has a negative entry and phase1 = 0");
+  if (arts > 0 && !opt.phase1) return fail(SIMPLEX_E_NEG_RHS, "b has a negative entry and phase1 = 0");
   if (overlap) {
     // the pipeline needs a second tableau buffer: fall back to select-then-pass in place when
     // two tableaux (+10 %) do not fit in the free device memory
@@ -832,51 +832,93 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
   return SIMPLEX_OK;
 }
 
-// Phase I -> Phase II on one column part (readings p3-p5 of DESIGN.md), between device loops:
+// Phase I -> Phase II (readings p3-p5 of DESIGN.md), between device loops, on every column part:
 // infeasible iff the Phase I optimum < -1e-7; each artificial still basic (rows ascending) is
 // pivoted out on its first column j < n+m with |T[i][j]| > tol_piv (a host-chosen pivot run
 // by the same update kernel); then the Phase II objective row is priced out on the device.
 simplex_err simplex_s::phase_transition() {
-  Slab& sl = slabs[0];
-  sx::SlabView& v = sl.v;
+  // Phase I -> Phase II on every column part (readings p3-p5): the verdict and the basis are
+  // replicated; each drive-out pivot's column is the first j < n+m with |T[i][j]| > tol_piv over
+  // ALL parts (each part's first candidate, then the minimum: an NCCL allreduce across ranks),
+  // gathered from its owner part and applied by the update kernel on every part
   RET(flush_all());
+  sx::SlabView& v0 = slabs[0].v;
   std::vector<int> basis((size_t)m);
-  CK(cudaMemcpyAsync(&h_state[2].p, v.T + v.w, sizeof(double), cudaMemcpyDeviceToHost, stream));
-  CK(cudaMemcpyAsync(basis.data(), v.basis, sizeof(int) * m, cudaMemcpyDeviceToHost, stream));
+  CK(cudaMemcpyAsync(&h_state[2].p, v0.T + v0.w, sizeof(double), cudaMemcpyDeviceToHost, stream));
+  CK(cudaMemcpyAsync(basis.data(), v0.basis, sizeof(int) * m, cudaMemcpyDeviceToHost, stream));
   CK(cudaStreamSynchronize(stream));
   phase = 2;
-  if (h_state[2].p < -1e-7) {
-    status = SIMPLEX_INFEASIBLE;
-    CK(sx::launch_set_status(v.st, SIMPLEX_INFEASIBLE, stream));
+  auto set_status_all = [&](int st) -> simplex_err {
+    for (auto& sl : slabs) CK(sx::launch_set_status(sl.v.st, st, stream));
     CK(cudaStreamSynchronize(stream));
     return SIMPLEX_OK;
+  };
+  if (h_state[2].p < -1e-7) {
+    status = SIMPLEX_INFEASIBLE;
+    return set_status_all(SIMPLEX_INFEASIBLE);
   }
-  std::vector<double> row((size_t)(n + m));
+  const bool multi = nparts > 1;
+  if (multi && !d_fcol) {                                // the drive-out column, gathered
+    RET(dalloc(&d_fcol, (size_t)m + 1));
+    RET(dalloc(&d_fj, 1));
+  }
+  double* d_col = d_fcol;
+  long long* d_j = d_fj;
+  std::vector<double> row;
   for (long long i = 1; i <= m; ++i) {
     if (basis[i - 1] < n + m) continue;
-    CK(cudaMemcpyAsync(row.data(), v.T + i * v.ld, sizeof(double) * (n + m), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    long long j = -1;
-    for (long long q = 0; q < n + m; ++q)
-      if (std::fabs(row[q]) > opt.tol_piv) { j = q; break; }
-    if (j < 0) continue;                                  // redundant row: artificial stays at 0
+    long long j = LLONG_MAX;
+    for (auto& sl : slabs) {                              // this rank's parts, ascending columns
+      const long long cols = std::max(0LL, std::min<long long>(sl.v.w, n + m - sl.v.c0));
+      if (cols == 0 || j != LLONG_MAX) continue;
+      row.resize((size_t)cols);
+      CK(cudaMemcpyAsync(row.data(), sl.v.T + i * sl.v.ld, sizeof(double) * cols, cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      for (long long q = 0; q < cols; ++q)
+        if (std::fabs(row[(size_t)q]) > opt.tol_piv) { j = sl.v.c0 + q; break; }
+    }
+    if (nranks > 1) {                                     // the first over all ranks
+      CK(cudaMemcpyAsync(d_j, &j, sizeof(j), cudaMemcpyHostToDevice, stream));
+      NK(ncclAllReduce(d_j, d_j, 1, ncclInt64, ncclMin, comm, stream));
+      CK(cudaMemcpyAsync(&j, d_j, sizeof(j), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+    }
+    if (j == LLONG_MAX) continue;                         // redundant row: artificial stays at 0
     if (it >= cap) {
       status = SIMPLEX_ITERATION_LIMIT;
-      CK(sx::launch_set_status(v.st, SIMPLEX_ITERATION_LIMIT, stream));
-      CK(cudaStreamSynchronize(stream));
-      return SIMPLEX_OK;
+      return set_status_all(SIMPLEX_ITERATION_LIMIT);
     }
-    CK(sx::launch_force(v, (int)i, (int)j, stream));
-    CK(sx::launch_update(v, sl.q, opt.tol_opt, sl.upd_grid, stream, false));
+    if (multi) {
+      // gather column j from its owner part (a slab of this rank, or a broadcast from its rank)
+      int64_t c0 = 0, w = 0;
+      long long owner = 0;
+      for (long long p = 0; p < nparts; ++p) {
+        RET(simplex_partition(n + m + arts, nparts, p, &c0, &w));
+        if (j >= c0 && j < c0 + w) { owner = p; break; }
+      }
+      const int orank = (int)(owner / nslabs);
+      if (orank == rank) {
+        const sx::SlabView& vo = slabs[(size_t)(owner % nslabs)].v;
+        CK(cudaMemcpy2DAsync(d_col, sizeof(double), vo.T + (j - vo.c0), sizeof(double) * vo.ld, sizeof(double),
+                             (size_t)m + 1, cudaMemcpyDeviceToDevice, stream));
+      }
+      if (nranks > 1) NK(ncclBroadcast(d_col, d_col, (size_t)m + 1, ncclFloat64, orank, comm, stream));
+    }
+    for (auto& sl : slabs) {
+      CK(sx::launch_force(sl.v, (int)i, (int)j, multi ? d_col : nullptr, stream));
+      CK(sx::launch_update(sl.v, sl.q, opt.tol_opt, sl.upd_grid, stream, false));
+    }
     RET(flush_all());
-    kernel_launches += 2;
+    kernel_launches += 2 * nslabs;
     basis[i - 1] = (int)j;
     ++it;
   }
-  CK(sx::launch_phase2_row0(v, n, stream));
-  CK(sx::launch_price0(v, opt.tol_opt, stream));
-  CK(sx::launch_set_status(v.st, SIMPLEX_RUNNING, stream));
-  kernel_launches += 3;
+  for (auto& sl : slabs) {
+    CK(sx::launch_phase2_row0(sl.v, n, stream));
+    CK(sx::launch_price0(sl.v, opt.tol_opt, stream));
+    CK(sx::launch_set_status(sl.v.st, SIMPLEX_RUNNING, stream));
+  }
+  kernel_launches += 3 * nslabs;
   CK(cudaStreamSynchronize(stream));
   status = SIMPLEX_RUNNING;
   return SIMPLEX_OK;

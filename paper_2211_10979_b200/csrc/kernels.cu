@@ -274,20 +274,23 @@ __global__ void __launch_bounds__(kThreads) k_phase2_row0(SlabView s, long long 
   s.T[j] = acc;
   if (j == 0) {
     s.st->phase = 2;
-    s.st->pw = (int)(n + s.rows - 1 - s.c0 < s.w ? n + s.rows - 1 - s.c0 : s.w);   // no artificials
+    const long long nm = n + s.rows - 1 - s.c0;   // this part's columns below n+m: no artificials
+    s.st->pw = (int)(nm < 0 ? 0 : nm < s.w ? nm : s.w);
   }
 }
 
-// Host-chosen pivot (Phase I drive-out, reading p4): stage column k, set the loop state so
-// k_update applies pivot (r, k) exactly like a selected one (trace, basis, counter).
-__global__ void __launch_bounds__(kThreads) k_force(SlabView s, int r, int k) {
+// Host-chosen pivot (Phase I drive-out, reading p4): stage column k (global index; `col` = that
+// column gathered from its owner part, or NULL: the local column k of a single part), set the loop
+// state so k_update applies pivot (r, k) exactly like a selected one (trace, basis, counter).
+__global__ void __launch_bounds__(kThreads) k_force(SlabView s, int r, int k, const double* __restrict__ col) {
   DevState* st = s.st;
-  for (int i = threadIdx.x; i < s.rows; i += blockDim.x) s.col[i] = s.T[(long long)i * s.ld + k];
+  for (int i = threadIdx.x; i < s.rows; i += blockDim.x) s.col[i] = col ? col[i] : s.T[(long long)i * s.ld + k];
+  __syncthreads();
   if (threadIdx.x == 0) {
     const long long it = st->it;
     st->r = r;
     st->k = k;
-    st->p = s.T[(long long)r * s.ld + k];
+    st->p = s.col[r];
     st->go = 1;
     st->pend_r = r;
     s.basis[r - 1] = k;
@@ -1716,8 +1719,8 @@ cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st) 
   SX_CHECK_LAUNCH();
 }
 
-cudaError_t launch_force(const SlabView& s, int r, int k, cudaStream_t st) {
-  k_force<<<1, kThreads, 0, st>>>(s, r, k);
+cudaError_t launch_force(const SlabView& s, int r, int k, const double* col, cudaStream_t st) {
+  k_force<<<1, kThreads, 0, st>>>(s, r, k, col);
   SX_CHECK_LAUNCH();
 }
 

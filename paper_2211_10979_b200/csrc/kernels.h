@@ -45,7 +45,7 @@ cudaError_t launch_update_s(int cfg, const SlabView& s, int S, const double* src
                             int Gr, int cw, cudaStream_t st, bool pdl);
 cudaError_t launch_phase1_row0(const SlabView& s, cudaStream_t st);
 cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st);
-cudaError_t launch_force(const SlabView& s, int r, int k, cudaStream_t st);
+cudaError_t launch_force(const SlabView& s, int r, int k, const double* col, cudaStream_t st);
 cudaError_t launch_set_status(DevState* d, int status, cudaStream_t st);
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st);
 cudaError_t launch_extract(const SlabView& s, long long n, double* x, double* y, double* obj, cudaStream_t st);

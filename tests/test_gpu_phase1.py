@@ -10,8 +10,9 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 PATHS = [dict(lookahead=1), dict(lookahead=4), dict(lookahead=16), dict(lookahead=16, overlap=False),
-         dict(lookahead=32)]
-PATH_IDS = ["pass1", "look4", "look16", "look16serial", "pair32"]
+         dict(lookahead=32), dict(lookahead=1, virtual_ranks=3), dict(lookahead=16, virtual_ranks=2),
+         dict(lookahead=8, virtual_ranks=3, exchange=2)]
+PATH_IDS = ["pass1", "look4", "look16", "look16serial", "pair32", "slabs3", "mpart2", "mpart3peer"]
 
 
 @pytest.fixture(scope="module")
@@ -21,6 +22,8 @@ def sx(cuda_device):
 
 
 def gpu(sx, A, b, c, **kw):
+    if "virtual_ranks" in kw:                      # at most one part per column (n + m of them)
+        kw["virtual_ranks"] = min(kw["virtual_ranks"], A.shape[0] + A.shape[1])
     with sx.Simplex(A, b, c, **kw) as s:
         st = s.solve()
         x, y, obj, piv, _ = s.solution()
@@ -100,9 +103,8 @@ def test_options_and_errors(sx):
     with pytest.raises(sx.SimplexError) as e:
         sx.Simplex(A, b, c, phase1=False)
     assert e.value.code == sx.E_NEG_RHS
-    with pytest.raises(sx.SimplexError) as e:
-        sx.Simplex(A, b, c, virtual_ranks=2, lookahead=1)
-    assert e.value.code == sx.E_NEG_RHS
+    with sx.Simplex(A, b, c, virtual_ranks=2, lookahead=1) as s:   # Phase I on several parts
+        assert s.solve() == sx.OPTIMAL
     with sx.Simplex(A, b, c) as s:                 # reset with a different sign pattern count
         with pytest.raises(sx.SimplexError) as e:
             s.reset(A, np.array([4.0, 1.0]), c)
