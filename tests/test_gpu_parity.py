@@ -193,6 +193,44 @@ def test_errors(sx):
     assert e.value.code == -1
 
 
+@pytest.mark.parametrize("seed", [2, 3, 4, 5])
+def test_dense_1000_seeds_default_path(sx, seed):
+    """SURVEY.md §8(d) seeds of the 1000x1000 config through the library default (rank-16
+    look-ahead pipelined with the pass), against the oracle run live, plus the certificates
+    computed from the raw (A, b, c): primal feasibility, dual feasibility, strong duality."""
+    A, b, c = lpgen.dense_lp(1000, 1000, seed)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    g = gpu_solve(sx, A, b, c, lookahead=0)
+    assert_same(g, o)
+    x, y, obj = g["x"], g["y"], g["obj"]
+    assert np.max(A @ x - b) <= 1e-6 and np.min(x) >= -1e-9
+    assert np.min(y) >= -1e-7 and np.min(A.T @ y - c) >= -1e-6
+    assert abs(c @ x - b @ y) <= 1e-9 * max(1.0, abs(obj))
+
+
+@pytest.mark.parametrize("key", [(4000, 4000, 2), (4000, 4000, 3), (8000, 8000, 2)])
+def test_golden_more_seeds_default_path(sx, key):
+    """The other §8(d) seeds of the 4000^2 / 8000^2 configs (goldens written by
+    scripts/make_golden.py from the oracle alone) through the bench's launch configuration."""
+    path = os.path.join(GOLDEN_DIR, "dense_%dx%d_s%d.npz" % key)
+    if not os.path.exists(path):
+        pytest.skip("golden file not generated: " + os.path.basename(path))
+    g = np.load(path)
+    A, b, c = lpgen.dense_lp(*key)
+    with sx.Simplex(A, b, c) as s:
+        st = s.solve()
+        x, y, obj, piv, _ = s.solution()
+        k, r = s.trace()
+        h = s.tableau_hash()
+    assert st == int(g["status"]) and piv == int(g["pivots"])
+    assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+    assert obj == float(g["objective"]) and np.array_equal(y, g["y"])
+    xs = np.zeros(key[1])
+    xs[g["x_idx"]] = g["x_val"]
+    assert np.array_equal(x, xs)
+    assert h == int(g["tableau_hash"])
+
+
 @pytest.mark.parametrize("key", [(1000, 1000, 1), (4000, 4000, 1), (8000, 8000, 1)])
 def test_golden_full_size(sx, key):
     """Bench-size configs against tests/golden (written by scripts/make_golden.py, oracle only)."""
