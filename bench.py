@@ -434,7 +434,10 @@ def main():
                          "pivots_per_launch": look,
                          "effective_gbs_per_pivot": st.bytes_per_pivot * pivs / (loop_ms / 1e3) / 1e9
                          if loop_ms > 0 else None,
-                         "single_pass": single, "pass_alone": alone},
+                         "single_pass": single, "pass_alone": alone,
+                         "note": ("tableau resident in L2 (%.0f MB per buffer < %d MB L2): the pass runs from L2, "
+                                  "so its fraction of the HBM peak is not a roofline" % (tableau_bytes / 1e6, l2 >> 20))
+                         if 2 * tableau_bytes < l2 else None},
             "cpu_baseline": cpu,
             "e2e": {"value": piv_e2e / (e2e_ms / 1e3), "unit": "pivots/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms": e2e_ms,
