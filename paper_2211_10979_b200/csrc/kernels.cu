@@ -962,6 +962,9 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
   double* __restrict__ prowO = s.prowS + (long long)bown * kMaxLook * ld;
   const double* __restrict__ colP = s.colS + (bpre >= 0 ? bpre : 0) * kMaxLook;
   const double* __restrict__ prowP = s.prowS + (long long)(bpre >= 0 ? bpre : 0) * kMaxLook * ld;
+  // transposed copies [t][row] of both banks: per-row chain loads coalesce across a warp
+  double* __restrict__ colTo = s.colT + (size_t)bown * kMaxLook * rows;
+  const double* __restrict__ colTp = s.colT + (size_t)(bpre >= 0 ? bpre : 0) * kMaxLook * rows;
   double* __restrict__ R0 = s.R0;
   double* __restrict__ RHS = s.RHS;
   long long it = st->it;
@@ -1020,16 +1023,17 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
     // Step 2 over all rows; the rhs gets the previous pivot first (at t = 0 of a pipelined
     // block: the previous block's last pivot)
     const int r_prev = t > 0 ? st->rsb[bown][t - 1] : spre > 0 ? sh_rp[spre - 1] : -1;
-    const double* c_prev = t > 0 ? colO + t - 1 : colP + (spre > 0 ? spre - 1 : 0);
+    const double* c_prev = t > 0 ? colTo + (size_t)(t - 1) * rows : colTp + (size_t)(spre > 0 ? spre - 1 : 0) * rows;
     const double pw_prev = r_prev < 0 ? 0.0
                            : __ldcg((t > 0 ? prowO + (long long)(t - 1) * ld : prowP + (long long)(spre - 1) * ld) + w);
     Cand rb = cand_none();
     for (long long i = gtid; i < rows; i += gthreads) {
       double h = RHS[i];
-      if (r_prev >= 0) h = (i == r_prev) ? pw_prev : __fma_rn(-c_prev[i * kColS], pw_prev, h);
+      if (r_prev >= 0) h = (i == r_prev) ? pw_prev : __fma_rn(-c_prev[i], pw_prev, h);
       RHS[i] = h;
       const double x = xget(q, 2 + i);
-      colO[i * kColS + t] = x;
+      colO[i * kColS + t] = x;                         // (row-major: the pass's TMA rows)
+      colTo[(size_t)t * rows + i] = x;
       if (i >= 1 && x > tol_piv) {
         int basic = 0;
         if (s.rule) basic = __ldcg(s.basis + i - 1);
@@ -1128,14 +1132,14 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
 #pragma unroll
       for (int u = 0; u < kMaxLook; ++u) {
         if (u < spre) {
-          const double cq = colP[i * kColS + u];
+          const double cq = colTp[(size_t)u * rows + i];
           x = (marked && i == sh_rp[u]) ? qk[u] : __fma_rn(-cq, qk[u], x);
         }
       }
 #pragma unroll
       for (int u = 0; u < kMaxLook; ++u) {
         if (u < nu) {
-          const double cu = colO[i * kColS + u];
+          const double cu = colTo[(size_t)u * rows + i];
           x = (marked && i == sh_r[u]) ? pk[u] : __fma_rn(-cu, pk[u], x);
         }
       }
