@@ -342,9 +342,12 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
         const char* e = std::getenv("SIMPLEX_NO_MBLOCK");
         mblock = !(e && e[0] == '1') && sx::mblock_max_clusters(sl.look_grid, v.rows) >= nslabs;
         if (mblock && opt.overlap != 0) {
+          // pipelined only up to 2.5 GB of slab stream per block: beyond it the one-GPU emulation
+          // measured the selection starved by the concurrent passes
           size_t free_b = 0, total_b = 0;
           CK(cudaMemGetInfo(&free_b, &total_b));
-          mpipe = 2.2 * 8.0 * (double)v.rows * (double)v.ld * nslabs <= (double)free_b;
+          mpipe = 2.2 * 8.0 * (double)v.rows * (double)v.ld * nslabs <= (double)free_b &&
+                  16.0 * (double)v.rows * (double)v.ld <= 2.5e9;
         }
       }
       // k_update_s: column chunks of cw doubles x row groups; all CTAs resident
