@@ -32,24 +32,31 @@ TOL_OPT = 1e-7      # SURVEY.md §8(c) c3 / SPEC.md:110
 TOL_PIV = 1e-10     # c5 / SPEC.md:110
 
 
-def build(force: bool = False) -> str:
-    """Compile simplex_oracle.c -> liboracle.so (gcc, -O2 -ffp-contract=off)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+
+
+def build(force: bool = False, parallel: bool = False) -> str:
+    """Compile simplex_oracle.c -> liboracle.so (gcc, -O2 -ffp-contract=off).
+    parallel=True builds liboracle_omp.so: the same source with -fopenmp, which
+    splits only or_pivot's independent row loop (bitwise identical results)."""
+    out = _LIB_OMP if parallel else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
         cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-march=x86-64-v3",
-               "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
+               "-fPIC", "-shared"] + (["-fopenmp"] if parallel else []) + \
+              ["-o", out + ".tmp", _SRC, "-lm"]
         subprocess.check_call(cmd)
-        os.replace(_LIB + ".tmp", _LIB)
-    return _LIB
+        os.replace(out + ".tmp", out)
+    return out
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        build()
-        L = C.CDLL(_LIB)
+def lib(parallel: bool = False):
+    """The oracle library; parallel=True -> the row-parallel -fopenmp build
+    (threads from OMP_NUM_THREADS)."""
+    if parallel not in _libs:
+        L = C.CDLL(build(parallel=parallel))
         i64, dp, ip = C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_int64)
         L.or_build.argtypes = [i64, i64, dp, dp, dp, dp, ip]
         L.or_build.restype = C.c_int
@@ -79,8 +86,11 @@ def lib():
         L.or_solve_2phase.restype = C.c_int
         L.or_brute_force.argtypes = [i64, i64, dp, dp, dp, C.c_double, dp, dp]
         L.or_brute_force.restype = C.c_int
-        _lib = L
-    return _lib
+        L.or_iterate.argtypes = [i64, i64, dp, ip, C.c_double, C.c_double, i64, i64, C.c_int,
+                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), i64, ip, dp, dp]
+        L.or_iterate.restype = C.c_int
+        _libs[parallel] = L
+    return _libs[parallel]
 
 
 def _dp(a):
@@ -187,8 +197,9 @@ DANTZIG, BLAND = 0, 1
 
 
 def solve(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, stop_after=-1,
-          trace_cap=None, keep_tableau=False, rule=DANTZIG) -> Result:
-    """Run the oracle (§III Steps Init/1/2/3/Iterate); rule DANTZIG or BLAND."""
+          trace_cap=None, keep_tableau=False, rule=DANTZIG, parallel=False) -> Result:
+    """Run the oracle (§III Steps Init/1/2/3/Iterate); rule DANTZIG or BLAND.
+    parallel=True runs the row-parallel build (same bits, see build())."""
     A, b, c = _f64(A), _f64(b), _f64(c)
     m, n = A.shape
     if trace_cap is None:
@@ -201,7 +212,7 @@ def solve(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, stop_after
     obj, piv, st = C.c_double(), C.c_int64(), C.c_int()
     T = np.empty((m + 1, n + m + 1)) if keep_tableau else None
     basis = np.empty(m, dtype=np.int64) if keep_tableau else None
-    err = lib().or_solve_rule(m, n, _dp(A), _dp(b), _dp(c), tol_opt, tol_piv, max_pivots, stop_after, rule,
+    err = lib(parallel).or_solve_rule(m, n, _dp(A), _dp(b), _dp(c), tol_opt, tol_piv, max_pivots, stop_after, rule,
                          tk.ctypes.data_as(C.POINTER(C.c_int32)),
                          tr.ctypes.data_as(C.POINTER(C.c_int32)), trace_cap,
                          _dp(x), _dp(y), C.byref(obj), C.byref(piv), C.byref(st),
@@ -211,6 +222,32 @@ def solve(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, stop_after
     npiv = piv.value
     keep = min(npiv, trace_cap)
     return Result(st.value, npiv, obj.value, x, y, tk[:keep].copy(), tr[:keep].copy(), T, basis)
+
+
+def iterate(T, basis, it, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, cap=None, stop_at=-1,
+            rule=DANTZIG, parallel=False):
+    """Continue the Iterate loop in place on a built tableau T (as from
+    build_tableau) and basis, after ``it`` pivots already done.  Returns
+    (status, total pivots, trace_k, trace_r) with the trace of THIS call only; a
+    RUNNING status means stop_at was reached and a later call resumes the identical
+    sequence.  cap defaults to 20(m+n) (reading c12)."""
+    assert T.dtype == np.float64 and T.flags.c_contiguous and basis.dtype == np.int64
+    m = T.shape[0] - 1
+    n = T.shape[1] - m - 1
+    if cap is None:
+        cap = 20 * (m + n)
+    tcap = max(1, (stop_at - it) if stop_at >= 0 else cap - it + 1)
+    tk = np.zeros(tcap, dtype=np.int32)
+    tr = np.zeros(tcap, dtype=np.int32)
+    itc = C.c_int64(it)
+    col, prow = np.empty(m + 1), np.empty(T.shape[1])
+    st = lib(parallel).or_iterate(m, n, _dp(T), basis.ctypes.data_as(C.POINTER(C.c_int64)),
+                                  tol_opt, tol_piv, cap, stop_at, rule,
+                                  tk.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  tr.ctypes.data_as(C.POINTER(C.c_int32)), tcap,
+                                  C.byref(itc), _dp(col), _dp(prow))
+    done = itc.value - it
+    return int(st), itc.value, tk[:done].copy(), tr[:done].copy()
 
 
 def solve_2phase(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, rule=DANTZIG,

@@ -14,6 +14,7 @@
  *   or_price    Step 1, entering variable (§IV Step 1)
  *   or_ratio    Step 2, minimum ratio test
  *   or_pivot    Step 3, pivoting
+ *   or_iterate  the Iterate loop on a built tableau, resumable
  *   or_solve    Iterate/Finalization
  *   or_extract  read x, y, objective off the final tableau
  *   or_price_bland / or_ratio_bland / or_solve_rule  Bland's rule
@@ -33,7 +34,12 @@
  *             the cap check (-> ITERATION_LIMIT), then pivot
  *
  * Build: gcc -O2 -ffp-contract=off -fPIC -shared (no -ffast-math: the fma and
- * the division must be exactly the IEEE operations written here).
+ * the division must be exactly the IEEE operations written here).  The same
+ * source built with -fopenmp (liboracle_omp.so) splits only or_pivot's row loop
+ * across threads — every element still gets the same single fma — and is used
+ * only by scripts/make_golden.py for the configs a single thread cannot finish
+ * (SURVEY.md §8(d) "Oracle baseline"); tests/test_oracle_omp.py proves it bitwise
+ * equal to the single-thread build.
  *
  * Pins (tests/test_oracle_*.py): SPEC worked examples, textbook LPs,
  * brute-force vertex enumeration, Klee-Minty (2^n - 1 pivots, optimum 5^n),
@@ -154,6 +160,12 @@ void or_pivot(int64_t m, int64_t W, double *T, int64_t r, int64_t k, double *col
     const double p = T[r * W + k];
     for (int64_t i = 0; i <= m; i++) col[i] = T[i * W + k];
     for (int64_t j = 0; j < W; j++) prow[j] = T[r * W + j] / p;
+    /* Rows are independent (each element gets exactly one fma with operands fixed
+     * before the loop), so the optional -fopenmp build (liboracle_omp.so, used only
+     * by scripts/make_golden.py for the largest configs, SURVEY.md §8(d) "Oracle
+     * baseline") splits this loop across threads without changing a single bit;
+     * tests/test_oracle_omp.py proves it.  The default build ignores the pragma. */
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i <= m; i++) {
         if (i == r) continue;
         double *row = T + i * W;
@@ -184,6 +196,37 @@ void or_extract(int64_t m, int64_t n, const double *T, const int64_t *basis,
  * many pivots are done (prefix runs).  T_out (optional, (m+1)*W) receives the final
  * tableau; trace_k/trace_r (optional, capacity trace_cap) receive (k, r) per pivot
  * (k 0-based column, r 1-based row). */
+/* The Iterate loop on an already built (m+1) x W tableau T with basis:
+ * repeat Step 1 (-> OPTIMAL), Step 2 (-> UNBOUNDED), the cap check (-> ITERATION_LIMIT,
+ * reading c12), Step 3.  *it is the pivot counter: it enters with the pivots already
+ * done (0 for a fresh tableau) and leaves with the total; the cap applies to the total.
+ * stop_at >= 0 returns OR_RUNNING when the total reaches stop_at (prefix and chunked
+ * runs: resuming with the same T, basis and *it continues the identical sequence).
+ * trace_k/trace_r[t] receive the (k, r) of the t-th pivot OF THIS CALL (t < trace_cap).
+ * col/prow are caller scratch of m+1 and W doubles.  rule 0: Dantzig (readings c1-c4);
+ * rule 1: Bland (or_price_bland / or_ratio_bland). */
+int or_iterate(int64_t m, int64_t n, double *T, int64_t *basis, double tol_opt, double tol_piv,
+               int64_t cap, int64_t stop_at, int rule, int32_t *trace_k, int32_t *trace_r,
+               int64_t trace_cap, int64_t *it, double *col, double *prow)
+{
+    const int64_t W = n + m + 1, it0 = *it;
+    for (;;) {
+        if (stop_at >= 0 && *it == stop_at) return OR_RUNNING;
+        const int64_t k = rule == 1 ? or_price_bland(T, n + m, tol_opt)  /* Step 1 */
+                                    : or_price(T, n + m, tol_opt, NULL);
+        if (k < 0) return OR_OPTIMAL;
+        const int64_t r = rule == 1 ? or_ratio_bland(m, W, T, k, tol_piv, basis, NULL)  /* Step 2 */
+                                    : or_ratio(m, W, T, k, tol_piv, NULL);
+        if (r < 0) return OR_UNBOUNDED;
+        if (*it == cap) return OR_ITERATION_LIMIT;
+        or_pivot(m, W, T, r, k, col, prow);                                /* Step 3 */
+        basis[r - 1] = k;
+        const int64_t t = *it - it0;
+        if (trace_k && t < trace_cap) { trace_k[t] = (int32_t)k; trace_r[t] = (int32_t)r; }
+        (*it)++;
+    }
+}
+
 /* rule 0: Dantzig (readings c1-c4); rule 1: Bland (or_price_bland / or_ratio_bland). */
 int or_solve_rule(int64_t m, int64_t n, const double *A, const double *b, const double *c,
                   double tol_opt, double tol_piv, int64_t max_pivots, int64_t stop_after, int rule,
@@ -209,21 +252,8 @@ int or_solve_rule(int64_t m, int64_t n, const double *A, const double *b, const 
     }
     const int64_t cap = max_pivots > 0 ? max_pivots : 20 * (m + n);
     int64_t it = 0;
-    int status = OR_RUNNING;
-    for (;;) {
-        if (stop_after >= 0 && it == stop_after) { status = OR_RUNNING; break; }
-        const int64_t k = rule == 1 ? or_price_bland(T, n + m, tol_opt)  /* Step 1 */
-                                    : or_price(T, n + m, tol_opt, NULL);
-        if (k < 0) { status = OR_OPTIMAL; break; }
-        const int64_t r = rule == 1 ? or_ratio_bland(m, W, T, k, tol_piv, basis, NULL)  /* Step 2 */
-                                    : or_ratio(m, W, T, k, tol_piv, NULL);
-        if (r < 0) { status = OR_UNBOUNDED; break; }
-        if (it == cap) { status = OR_ITERATION_LIMIT; break; }
-        or_pivot(m, W, T, r, k, col, prow);                                /* Step 3 */
-        basis[r - 1] = k;
-        if (trace_k && it < trace_cap) { trace_k[it] = (int32_t)k; trace_r[it] = (int32_t)r; }
-        it++;
-    }
+    const int status = or_iterate(m, n, T, basis, tol_opt, tol_piv, cap, stop_after, rule,
+                                  trace_k, trace_r, trace_cap, &it, col, prow);
     or_extract(m, n, T, basis, x, y, obj);
     if (basis_out) memcpy(basis_out, basis, sizeof(int64_t) * (size_t)m);
     if (pivots_out) *pivots_out = it;
