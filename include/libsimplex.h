@@ -122,8 +122,18 @@ typedef struct {
                                releases a flag there — no collective launch per pivot), else
                                NCCL; on virtual slabs, plain stores into the shared buffer;
                                1 = one ncclAllGather per selected pivot (virtual slabs: plain
-                               stores); 2 = the peer-memory protocol (also on virtual slabs:
-                               its test path) or SIMPLEX_E_CUDA.  Bitwise identical results. */
+                               stores; ONE column part: the same gather through a 1-rank NCCL
+                               communicator — the NCCL data flow testable on one GPU);
+                               2 = the peer-memory protocol (also on virtual slabs: its test
+                               path) or SIMPLEX_E_CUDA; 3 = as 2 but one k_mlook launch per
+                               selected pivot instead of one k_mblock per block (test path of
+                               the per-pivot protocol).  > 3 -> SIMPLEX_E_ARG.  Bitwise
+                               identical results.                                          */
+    int32_t  exchange_timeout_ms; /* peer-memory exchange: a poll for a peer's candidate
+                               column gives up after this long (<= 0: 30000), stops the loop,
+                               returns SIMPLEX_E_NCCL and latches the handle (every later call
+                               except destroy returns SIMPLEX_E_STATE).  Raise it when ranks may
+                               launch far apart (e.g. under a profiler's kernel replay).    */
 } simplex_options;
 
 typedef struct {

@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("SIMPLEX_LIB") or os.path.join(_PKG, "libsimplex.so")   # SIMPLEX_LIB: experiment variants
+LIB_PATH = os.path.join(_PKG, "libsimplex.so")
 
 OK = 0
 E_ARG, E_NONFINITE, E_NEG_RHS, E_OOM, E_CUDA, E_NCCL, E_STATE = -1, -2, -3, -4, -5, -6, -7
@@ -45,7 +45,7 @@ class Options(C.Structure):
                 ("stream", C.c_void_p), ("virtual_ranks", C.c_int32), ("segment_pivots", C.c_int32),
                 ("time_kernels", C.c_int32), ("lookahead", C.c_int32),
                 ("pivot_rule", C.c_int32), ("phase1", C.c_int32), ("overlap", C.c_int32),
-                ("exchange", C.c_int32)]
+                ("exchange", C.c_int32), ("exchange_timeout_ms", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -99,6 +99,16 @@ def lib():
     return _lib
 
 
+def use_library(path: str) -> None:
+    """Experiment scripts only (scripts/_experiment.py): load `path` — a build with the
+    SIMPLEX_* environment hooks compiled in — instead of the product libsimplex.so.
+    Must be called before the library is first loaded."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("libsimplex is already loaded from " + LIB_PATH)
+    LIB_PATH = path
+
+
 def _check(code):
     if code != OK:
         raise SimplexError(code, lib().simplex_last_error().decode())
@@ -137,27 +147,41 @@ def version() -> str:
     return lib().simplex_version().decode()
 
 
-def _ptr(a, keep):
-    """Device pointer of a CUDA tensor, or host pointer of a C-contiguous float64 array."""
+def _ptr(a, keep, numel, device=None):
+    """Device pointer of a CUDA tensor (float64, contiguous, on the handle's device), or host
+    pointer of a C-contiguous float64 copy of anything array-like; exactly `numel` elements."""
     if a is None:
         return None
     if hasattr(a, "is_cuda") and hasattr(a, "data_ptr"):
         import torch
         if a.is_cuda:
-            assert a.dtype == torch.float64 and a.is_contiguous(), "CUDA inputs must be contiguous float64"
+            if a.dtype != torch.float64 or not a.is_contiguous():
+                raise ValueError("CUDA inputs must be contiguous float64 tensors")
+            if a.numel() != numel:
+                raise ValueError(f"expected {numel} elements, got {a.numel()}")
+            if device is not None and device >= 0 and a.device.index != device:
+                raise ValueError(f"CUDA input on device {a.device.index}, handle on device {device}")
             keep.append(a)
             return C.c_void_p(a.data_ptr())
         a = a.numpy()
     arr = np.ascontiguousarray(a, dtype=np.float64)
+    if arr.size != numel:
+        raise ValueError(f"expected {numel} elements, got {arr.size}")
     keep.append(arr)
     return C.c_void_p(arr.ctypes.data)
 
 
-def _current_stream():
+def _shape(a):
+    return tuple(int(v) for v in a.shape)
+
+
+def _current_stream(device):
+    """torch's current stream ON THE HANDLE'S DEVICE (None without an initialised CUDA context)."""
     try:
         import torch
         if torch.cuda.is_available() and torch.cuda.is_initialized():
-            return torch.cuda.current_stream().cuda_stream
+            dev = torch.cuda.current_device() if device is None or device < 0 else device
+            return torch.cuda.current_stream(dev).cuda_stream
     except Exception:
         pass
     return None
@@ -175,7 +199,11 @@ class Simplex:
                  device=None, group=None, virtual_ranks=1, segment_pivots=0, time_kernels=False,
                  lookahead=0, pivot_rule=DANTZIG, phase1=True, overlap=True, stream=None, exchange=0):
         L = lib()
-        m, n = (int(A.shape[0]), int(A.shape[1]))
+        if len(_shape(A)) != 2:
+            raise ValueError("A must be a 2-D (m, n) array")
+        m, n = _shape(A)
+        if _shape(b) != (m,) or _shape(c) != (n,):
+            raise ValueError(f"b must have shape ({m},) and c shape ({n},); got {_shape(b)}, {_shape(c)}")
         o = default_options()
         o.tol_opt, o.tol_piv, o.max_pivots = tol_opt, tol_piv, max_pivots
         o.record_trace = 1 if record_trace else 0
@@ -188,7 +216,7 @@ class Simplex:
         o.phase1 = 1 if phase1 else 0
         o.overlap = 1 if overlap else 0
         o.exchange = int(exchange)
-        s = stream if stream is not None else _current_stream()
+        s = stream if stream is not None else _current_stream(o.device)
         o.stream = s if s else None
         self._idbuf = None
         if group is not None:
@@ -202,8 +230,10 @@ class Simplex:
         self.nranks, self.rank = o.nranks, o.rank
         keep = []
         h = C.c_void_p()
-        _check(L.simplex_create(C.byref(h), m, n, _ptr(A, keep), _ptr(b, keep), _ptr(c, keep), C.byref(o)))
+        _check(L.simplex_create(C.byref(h), m, n, _ptr(A, keep, m * n, o.device), _ptr(b, keep, m, o.device),
+                                _ptr(c, keep, n, o.device), C.byref(o)))
         self._h = h
+        self.device = self._device_of_handle(o.device)
 
     # --------------------------------------------------------------- lifecycle
     def close(self):
@@ -220,9 +250,24 @@ class Simplex:
         self.close()
 
     # --------------------------------------------------------------- calls
+    @staticmethod
+    def _device_of_handle(device):
+        if device is not None and device >= 0:
+            return device
+        try:
+            import torch
+            return torch.cuda.current_device()
+        except Exception:
+            return -1
+
     def reset(self, A, b, c):
+        """Rebuild from new data of the SAME shape (simplex_reset)."""
+        m, n = self.m, self.n
+        if _shape(A) != (m, n) or _shape(b) != (m,) or _shape(c) != (n,):
+            raise ValueError(f"reset needs A ({m}, {n}), b ({m},), c ({n},)")
         keep = []
-        _check(lib().simplex_reset(self._h, _ptr(A, keep), _ptr(b, keep), _ptr(c, keep)))
+        _check(lib().simplex_reset(self._h, _ptr(A, keep, m * n, self.device), _ptr(b, keep, m, self.device),
+                                   _ptr(c, keep, n, self.device)))
 
     def solve(self) -> int:
         st = C.c_int()
@@ -240,7 +285,8 @@ class Simplex:
         yo = np.empty(self.m) if y is None else y
         keep = []
         obj, piv, st = C.c_double(), C.c_int64(), C.c_int()
-        _check(lib().simplex_get_solution(self._h, _out_ptr(xo, keep), _out_ptr(yo, keep), C.byref(obj),
+        _check(lib().simplex_get_solution(self._h, _out_ptr(xo, keep, self.n, self.device),
+                                          _out_ptr(yo, keep, self.m, self.device), C.byref(obj),
                                           C.byref(piv), C.byref(st)))
         return xo, yo, obj.value, piv.value, st.value
 
@@ -272,12 +318,19 @@ class Simplex:
         return s
 
 
-def _out_ptr(a, keep):
+def _out_ptr(a, keep, numel, device):
+    """An output buffer: float64, contiguous, exactly `numel` elements (CUDA: on the handle's
+    device).  Anything else raises ValueError instead of becoming an out-of-bounds write."""
     if hasattr(a, "is_cuda") and hasattr(a, "data_ptr"):
-        assert a.is_contiguous()
+        import torch
+        if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() != numel:
+            raise ValueError(f"output must be a contiguous float64 tensor of {numel} elements")
+        if a.is_cuda and device is not None and device >= 0 and a.device.index != device:
+            raise ValueError(f"output on device {a.device.index}, handle on device {device}")
         keep.append(a)
         return C.c_void_p(a.data_ptr())
-    assert isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous and a.size == numel):
+        raise ValueError(f"output must be a C-contiguous float64 array of {numel} elements")
     return C.c_void_p(a.ctypes.data)
 
 

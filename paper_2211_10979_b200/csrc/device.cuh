@@ -81,6 +81,7 @@ struct XPeers {
   long long half;                      // values per parity (nparts * xstride)
   unsigned long long* x[kMaxPeers];    // gather buffers of every rank (LL words)
   const unsigned long long* mine;      // this rank's gather buffer
+  unsigned long long timeout_ns;       // a poll gives up after this long (options.exchange_timeout_ms)
 };
 
 struct SlabView {

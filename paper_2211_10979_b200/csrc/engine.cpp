@@ -129,12 +129,14 @@ struct simplex_s {
   bool look_cache = true;           // pipelined selection keeps the previous bank in shared memory
   int pass_cfg = 0;                 // k_update_s configuration (kernels.cu kPassCfgs)
   bool pdl = true;                  // programmatic dependent launch between pivot kernels
-  bool force_nccl = false;          // test hook: 1-rank NCCL exchange on one GPU
+  bool force_nccl = false;          // exchange = 1 on one part: 1-rank NCCL exchange on one GPU
   bool graphs_ready = false;
   cudaGraphExec_t seg[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> tev[2];
   // host view of the loop
   int status = SIMPLEX_RUNNING;
+  bool faulted = false;             // latched after an exchange timeout or a CUDA/NCCL error in
+                                    // the loop: every later call except destroy -> E_STATE
   int phase = 2;                    // 1 while the Phase I objective is being optimized
   long long it = 0;
   // stats
@@ -168,7 +170,7 @@ struct simplex_s {
   // graph steps per segment; the pipeline alternates two tableau buffers, so an even count
   // brings the tableau back to buffer 0 at every segment boundary
   bool time_pass() const {                     // the pipelined pass is timed on the device
-    static const bool time_sel = std::getenv("SIMPLEX_TIME_SELECT") != nullptr;
+    static const bool time_sel = sx::experiment_env("SIMPLEX_TIME_SELECT") != nullptr;
     return opt.time_kernels && (overlap || mpipe) && !time_sel;
   }
   int steps_per_segment() const {
@@ -230,12 +232,9 @@ struct simplex_s {
 // Rows with b_i < 0 (1-based, ascending) and their artificial index (reading p1).
 simplex_err simplex_s::scan_b(const double* b, std::vector<int>* art_of_row, std::vector<int>* neg) {
   std::vector<double> hb((size_t)m);
-  if (stream) {                                   // ordered after the caller's stream (enter())
-    CK(cudaMemcpyAsync(hb.data(), b, sizeof(double) * m, cudaMemcpyDefault, stream));
-    CK(cudaStreamSynchronize(stream));
-  } else {
-    CK(cudaMemcpy(hb.data(), b, sizeof(double) * m, cudaMemcpyDefault));
-  }
+  // ordered after the caller's stream: every caller runs enter() first
+  CK(cudaMemcpyAsync(hb.data(), b, sizeof(double) * m, cudaMemcpyDefault, stream));
+  CK(cudaStreamSynchronize(stream));
   art_of_row->assign((size_t)m, -1);
   neg->clear();
   for (long long i = 0; i < m; ++i)
@@ -260,9 +259,11 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   if (m + 1 > INT_MAX / 2 || n + m > INT_MAX / 2) return fail(SIMPLEX_E_ARG, "dimensions too large");
   cap = opt.max_pivots > 0 ? opt.max_pivots : 20 * (m + n);
   S = opt.segment_pivots > 0 ? opt.segment_pivots : 32;
-  if (const char* e = std::getenv("SIMPLEX_NO_PDL")) pdl = !(e[0] == '1');
-  if (const char* e = std::getenv("SIMPLEX_NO_LOOK_CACHE")) look_cache = !(e[0] == '1');   // experiment hook
-  if (const char* e = std::getenv("SIMPLEX_FORCE_NCCL")) force_nccl = (e[0] == '1') && nranks == 1 && nslabs == 1;
+  if (const char* e = sx::experiment_env("SIMPLEX_NO_PDL")) pdl = !(e[0] == '1');
+  if (const char* e = sx::experiment_env("SIMPLEX_NO_LOOK_CACHE")) look_cache = !(e[0] == '1');
+  // exchange = 1 on ONE column part: gather the candidate columns through a 1-rank NCCL
+  // communicator (the multi-GPU data flow, NCCL flavour, testable on one GPU)
+  force_nccl = opt.exchange == 1 && nranks == 1 && nslabs == 1;
   // 0 = automatic: rank-16 look-ahead on one column part, one pivot per pass otherwise
   // 0 = automatic: rank-16 look-ahead (one part: pipelined with the pass; several parts: one
   // exchange of candidate columns per selected pivot, then one pass per block)
@@ -273,12 +274,12 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   // 17..32: the pair schedule — two selections (bank 0, then bank 1 chaining bank 0) and ONE
   // pass applying both banks; select-then-pass (no pipeline)
   overlap = look > 1 && look <= sx::kMaxLook && opt.overlap != 0 && nparts == 1 && !force_nccl;
-  if (opt.exchange < 0 || opt.exchange > 2) return fail(SIMPLEX_E_ARG, "exchange must be 0, 1 or 2");
+  if (opt.exchange < 0 || opt.exchange > 3) return fail(SIMPLEX_E_ARG, "exchange must be 0, 1, 2 or 3");
   // multi-part look-ahead on several ranks: peer-memory exchange unless NCCL is asked for
   // (peer reachability is checked once the device is known); the 1-rank NCCL hook keeps NCCL
   // (one GPU, virtual slabs: only when asked for — there the protocol is pure overhead, the
   // stream already orders the parts; measured +6 us per k_mlook launch for the system fence)
-  p2p = look > 1 && nparts > 1 && !force_nccl && (opt.exchange == 2 || (opt.exchange == 0 && nranks > 1));
+  p2p = look > 1 && nparts > 1 && !force_nccl && (opt.exchange >= 2 || (opt.exchange == 0 && nranks > 1));
   if (p2p && nranks > kMaxPeersHost) return fail(SIMPLEX_E_ARG, "peer-memory exchange supports up to 8 ranks");
 
   int ndev = 0;
@@ -292,6 +293,10 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   }
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  user_stream = static_cast<cudaStream_t>(opt.stream);
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming));
+  RET(enter());                     // b may have been written on the caller's stream
   // Phase I (NEXT #2): one artificial column per row with b_i < 0
   std::vector<int> art_of_row;
   RET(scan_b(b, &art_of_row, &art_rows));
@@ -307,9 +312,6 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     if (2.2 * tab > (double)free_b) overlap = false;
   }
 
-  user_stream = static_cast<cudaStream_t>(opt.stream);
-  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-  CK(cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming));
   CK(cudaEventCreate(&ev_loop0));
   CK(cudaEventCreate(&ev_loop1));
   for (auto& e : ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -339,8 +341,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
         // rank per GPU; virtual slabs: nslabs clusters on this GPU, each on its own stream), else
         // one k_mlook per pivot (also SIMPLEX_NO_MBLOCK=1, experiment hook); pipelined with the
         // slab passes (overlap = 1) when two tableau buffers per slab fit
-        const char* e = std::getenv("SIMPLEX_NO_MBLOCK");
-        mblock = !(e && e[0] == '1') && sx::mblock_max_clusters(sl.look_grid, v.rows) >= nslabs;
+        mblock = opt.exchange != 3 && sx::mblock_max_clusters(sl.look_grid, v.rows) >= nslabs;
         if (mblock && opt.overlap != 0) {
           // pipelined only up to 2.5 GB of slab stream per block: beyond it the one-GPU emulation
           // measured the selection starved by the concurrent passes
@@ -360,7 +361,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       pass_cfg = sx::pass_cfg_choice(overlap || mpipe, 16.0 * v.rows * v.ld);   // bytes read + written per pass
       CK(sx::update_s_occupancy(pass_cfg, look, &occ, sx::update_s_smem(pass_cfg, cwmax, v.rows, look)));
       if (occ < 1) return fail(SIMPLEX_E_CUDA, "rank-s pass kernel cannot be resident");
-      const char* ps = getenv("SIMPLEX_PASS_SMS");          // experiment hook
+      const char* ps = sx::experiment_env("SIMPLEX_PASS_SMS");
       const long long slots = (long long)occ * (ps ? atoi(ps) : overlap ? sms - sl.look_grid
                                                                 : mpipe ? sms - nslabs * sl.look_grid : sms);
       const long long nc0 = (v.ld + cwmax - 1) / cwmax;
@@ -413,7 +414,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       RET(dalloc(&v.RHS, v.rows));
       RET(dalloc(&v.pcand, sl.look_grid));
       v.time_pass = time_pass() ? 1 : 0;
-      if (std::getenv("SIMPLEX_PROBE")) {                 // experiment hook: selection phase stamps
+      if (sx::experiment_env("SIMPLEX_PROBE")) {          // experiment hook: selection phase stamps
         RET(dalloc(&v.probe, (size_t)sx::kProbeSlots * 16 * sx::kProbeEv));
         CK(cudaMemset(v.probe, 0, sizeof(unsigned long long) * sx::kProbeSlots * 16 * sx::kProbeEv));
       }
@@ -492,7 +493,7 @@ simplex_err simplex_s::setup_p2p() {
       CK(cudaStreamSynchronize(stream));
     }
     if (!ok) {
-      if (opt.exchange == 2) return fail(SIMPLEX_E_CUDA, "exchange = 2 (peer memory) but a peer GPU is not reachable");
+      if (opt.exchange >= 2) return fail(SIMPLEX_E_CUDA, "exchange = 2/3 (peer memory) but a peer GPU is not reachable");
       p2p = false;
       RET(dalloc(&send, xstride));                        // NCCL allgather path
       return SIMPLEX_OK;
@@ -530,6 +531,7 @@ simplex_err simplex_s::setup_p2p() {
     xp.half = half;
     for (int r = 0; r < nranks; ++r) xp.x[r] = px[(size_t)r];
     xp.mine = xll;
+    xp.timeout_ns = 1000000ull * (unsigned long long)(opt.exchange_timeout_ms > 0 ? opt.exchange_timeout_ms : 30000);
   }
   return SIMPLEX_OK;
 }
@@ -659,7 +661,7 @@ simplex_err simplex_s::enqueue_pivot(int slot, int t) {
       // remaining SMs as soon as the cluster is resident (PDL; it does not wait for it).
       const int q = t & 1;
       double* buf[2] = {sl.v.T, sl.T2};
-      static const bool time_sel = std::getenv("SIMPLEX_TIME_SELECT") != nullptr;   // experiment hook
+      static const bool time_sel = sx::experiment_env("SIMPLEX_TIME_SELECT") != nullptr;   // experiment hook
       if (opt.time_kernels && !time_sel) {
         // the pass times itself on the device (SlabView::time_pass) so that it still runs
         // concurrently with the selection: the production launch sequence, no event nodes
@@ -797,10 +799,10 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
         }
       }
       if (hs.err & sx::kErrExchange) {
-        CK(cudaStreamSynchronize(stream));
-        status = SIMPLEX_RUNNING;
+        cudaStreamSynchronize(stream);
+        faulted = true;
         return fail(SIMPLEX_E_NCCL, "peer-memory exchange timed out: a peer did not publish its candidate "
-                                    "column within 30 s (the handle must be destroyed)");
+                                    "column within exchange_timeout_ms (the handle must be destroyed)");
       }
       seen = hs.it;
       status = hs.status;
@@ -936,7 +938,7 @@ simplex_err simplex_s::flush_all() {
 void simplex_s::release() {
   if (device >= 0) cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
-  if (const char* path = std::getenv("SIMPLEX_PROBE"))    // experiment hook: dump the stamps
+  if (const char* path = sx::experiment_env("SIMPLEX_PROBE"))   // experiment hook: dump the stamps
     if (!slabs.empty() && slabs[0].v.probe) {
       std::vector<unsigned long long> hp((size_t)sx::kProbeSlots * 16 * sx::kProbeEv);
       if (cudaMemcpy(hp.data(), slabs[0].v.probe, hp.size() * sizeof(hp[0]), cudaMemcpyDeviceToHost) == cudaSuccess)
@@ -969,6 +971,14 @@ void simplex_s::release() {
 }
 
 // ====================================================================== C ABI
+// Every call but destroy: a NULL handle is E_ARG; a handle latched after a fault in its device
+// loop (exchange timeout, CUDA or NCCL error) is E_STATE — its device state is undefined.
+#define HANDLE_OK(h)                                                                          \
+  do {                                                                                        \
+    if (!(h)) return fail(SIMPLEX_E_ARG, "NULL handle");                                      \
+    if ((h)->faulted) return fail(SIMPLEX_E_STATE, "the handle faulted earlier; destroy it");  \
+  } while (0)
+
 extern "C" {
 
 void simplex_default_options(simplex_options* o) {
@@ -1028,17 +1038,18 @@ simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* 
 
 simplex_err simplex_reset(simplex_t* h, const double* A, const double* b, const double* c) {
   g_err.clear();
-  if (!h) return fail(SIMPLEX_E_ARG, "NULL handle");
+  HANDLE_OK(h);
   DeviceGuard dg(h->device);
   return h->load(A, b, c);
 }
 
 simplex_err simplex_iterate(simplex_t* h, int64_t max_pivots, int64_t* pivots_done, simplex_status* st) {
   g_err.clear();
-  if (!h) return fail(SIMPLEX_E_ARG, "NULL handle");
+  HANDLE_OK(h);
   DeviceGuard dg(h->device);
   long long done = 0;
   simplex_err e = h->run(max_pivots, &done);
+  if (e == SIMPLEX_E_CUDA || e == SIMPLEX_E_NCCL) h->faulted = true;
   if (pivots_done) *pivots_done = done;
   if (st) *st = static_cast<simplex_status>(h->status);
   return e;
@@ -1049,7 +1060,7 @@ simplex_err simplex_solve(simplex_t* h, simplex_status* st) { return simplex_ite
 simplex_err simplex_get_solution(simplex_t* h, double* x, double* y, double* objective, int64_t* pivots,
                                  simplex_status* st) {
   g_err.clear();
-  if (!h) return fail(SIMPLEX_E_ARG, "NULL handle");
+  HANDLE_OK(h);
   DeviceGuard dg(h->device);
   RET(h->enter());
   RET(h->flush_all());
@@ -1073,7 +1084,7 @@ simplex_err simplex_get_solution(simplex_t* h, double* x, double* y, double* obj
 
 simplex_err simplex_get_trace(simplex_t* h, int32_t* k, int32_t* r, int64_t cap, int64_t* len) {
   g_err.clear();
-  if (!h) return fail(SIMPLEX_E_ARG, "NULL handle");
+  HANDLE_OK(h);
   DeviceGuard dg(h->device);
   const sx::SlabView& v = h->slabs[0].v;
   const long long n = std::min<long long>(std::min<long long>(h->it, v.trace_cap), std::max<int64_t>(cap, 0));
@@ -1089,7 +1100,8 @@ simplex_err simplex_get_trace(simplex_t* h, int32_t* k, int32_t* r, int64_t cap,
 
 simplex_err simplex_get_tableau(simplex_t* h, double* T_out, int64_t ld_out) {
   g_err.clear();
-  if (!h || !T_out) return fail(SIMPLEX_E_ARG, "NULL argument");
+  HANDLE_OK(h);
+  if (!T_out) return fail(SIMPLEX_E_ARG, "NULL argument");
   DeviceGuard dg(h->device);
   long long cols = 1;
   for (auto& sl : h->slabs) cols += sl.v.w;
@@ -1111,7 +1123,8 @@ simplex_err simplex_get_tableau(simplex_t* h, double* T_out, int64_t ld_out) {
 
 simplex_err simplex_tableau_hash(simplex_t* h, uint64_t* hash) {
   g_err.clear();
-  if (!h || !hash) return fail(SIMPLEX_E_ARG, "NULL argument");
+  HANDLE_OK(h);
+  if (!hash) return fail(SIMPLEX_E_ARG, "NULL argument");
   DeviceGuard dg(h->device);
   RET(h->enter());
   CK(cudaMemsetAsync(h->d_hash, 0, sizeof(unsigned long long), h->stream));

@@ -915,9 +915,11 @@ __device__ __forceinline__ void ll_store(unsigned long long* w, double x, unsign
   asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(w), "l"(lo), "l"(hi) : "memory");
 }
 // Polls until both words carry sequence number q.  A peer that never publishes (a dead rank)
-// must not hang the GPU: after 30 s the word is given up on, the handle's loop is stopped
-// (status kFault, err kErrExchange) and the host reports SIMPLEX_E_NCCL.
-__device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned int q, DevState* st) {
+// must not hang the GPU: after timeout_ns (options.exchange_timeout_ms, default 30 s) the word
+// is given up on, the handle's loop is stopped (status kFault, err kErrExchange), the host
+// reports SIMPLEX_E_NCCL and latches the handle (every later call but destroy: E_STATE).
+__device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned int q, DevState* st,
+                                          unsigned long long timeout_ns) {
   unsigned long long lo, hi, t0 = 0;
   for (unsigned int n = 0;; ++n) {
     asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(w) : "memory");
@@ -929,7 +931,7 @@ __device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned 
       if (*(volatile int*)&st->status == kFault) return 0.0;     // another thread gave up already
       if (t0 == 0) {
         t0 = now;
-      } else if (now - t0 > 30000000000ull) {
+      } else if (now - t0 > timeout_ns) {
         atomicOr(&st->err, kErrExchange);
         st->status = kFault;
         return 0.0;
@@ -978,7 +980,8 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
   const unsigned long long* xll = xp.n > 0 ? xp.mine + 2 * (long long)(t & 1) * xp.half : nullptr;
   // value e of part q's slot in the gathered buffer of this pivot
   auto xget = [&](int q, long long e) -> double {
-    return xll ? ll_load(xll + 2 * ((long long)q * xstride + e), xseq, st) : __ldcg(xin + (long long)q * xstride + e);
+    return xll ? ll_load(xll + 2 * ((long long)q * xstride + e), xseq, st, xp.timeout_ns)
+               : __ldcg(xin + (long long)q * xstride + e);
   };
   // pivot-row bitmap of both banks (own pivots 0..t-1)
   for (int q = threadIdx.x; q < (rows + 31) / 32; q += blockDim.x) piv_mark[q] = 0u;
@@ -1567,7 +1570,7 @@ int lookahead_cluster_size() {
   cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_lookahead, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLookCacheMax);
   cudaFuncSetAttribute(k_mlook, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  const char* e = std::getenv("SIMPLEX_LOOK_CLUSTER");   // experiment hook: cap the cluster size
+  const char* e = experiment_env("SIMPLEX_LOOK_CLUSTER");   // experiment hook: cap the cluster size
   const int cmax = e ? std::atoi(e) : 16;
   for (int c : {16, 8, 4, 2, 1}) {
     if (c > cmax) continue;
@@ -1644,7 +1647,7 @@ cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown
 struct PassCfg { int R, K; };
 static const PassCfg kPassCfgs[] = {{4, 12}, {4, 10}, {8, 5}, {6, 7}, {2, 16}, {4, 8}};
 int pass_cfg_choice(bool pipelined, double pass_bytes) {
-  const char* e = std::getenv("SIMPLEX_PASS_CFG");
+  const char* e = experiment_env("SIMPLEX_PASS_CFG");
   const int v = e ? std::atoi(e) : -1;
   if (v >= 0 && v < 6) return v;
   if (pipelined && pass_bytes < 1e9) return 4;     // selection-bound (4000^2: 210 us blocks, 104 us pass)

@@ -2,9 +2,24 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "device.cuh"
 
 namespace sx {
+
+// Experiment hooks (SIMPLEX_* environment variables used by scripts/ probes) exist only in
+// builds compiled with -DSIMPLEX_EXPERIMENTS (build.build(defines=["SIMPLEX_EXPERIMENTS"],
+// out=...)).  The product libsimplex.so never reads the environment: every behaviour of it
+// is chosen by simplex_options.
+inline const char* experiment_env(const char* name) {
+#ifdef SIMPLEX_EXPERIMENTS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 constexpr int kUpdateRows = 4;   // rows in flight per thread in k_update (measured)
 constexpr int kUpdateCtasPerSm = 4;

@@ -10,6 +10,8 @@ import torch  # noqa: E402
 
 import lpgen  # noqa: E402
 import paper_2211_10979_b200 as sx  # noqa: E402
+import _experiment  # noqa: E402
+_experiment.load()
 
 m, n = map(int, sys.argv[1].split("x"))
 piv = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
@@ -31,9 +33,9 @@ def timed(label, **kw):
         print(f"{label}: {us / done:.1f} us/pivot, {us / (done / 16):.1f} us/block")
 
 
-if os.environ.get("SIMPLEX_FORCE_NCCL"):
-    timed("nccl 1-rank look16")
-    timed("nccl 1-rank one pivot per pass", lookahead=1)
+if "--nccl" in sys.argv:
+    timed("nccl 1-rank look16", exchange=1)
+    timed("nccl 1-rank one pivot per pass", lookahead=1, exchange=1)
     sys.exit(0)
 timed("1 part, pipelined")
 for P in (2, 4):

@@ -8,6 +8,8 @@ if len(sys.argv) > 2:
     import torch
     import lpgen
     import paper_2211_10979_b200 as sx
+    import _experiment
+    _experiment.load()
     m, n = map(int, sys.argv[1].split("x"))
     torch.cuda.set_device(0)
     A, b, c = lpgen.dense_lp(m, n, 1)

@@ -17,6 +17,8 @@ import torch  # noqa: E402
 
 import lpgen  # noqa: E402
 import paper_2211_10979_b200 as sx  # noqa: E402
+import _experiment  # noqa: E402
+_experiment.load()
 
 m, n = map(int, sys.argv[1].split("x"))
 piv = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 2000

@@ -105,9 +105,9 @@ def test_argument_errors_before_any_device_work():
     bad.struct_size = 7
     assert sx.lib().simplex_create(C.byref(h), 2, 2, A.ctypes.data, b.ctypes.data, c.ctypes.data,
                                    C.byref(bad)) == sx.E_ARG
-    # option values rejected before any device work: exchange outside 0..2, lookahead > 32, the
+    # option values rejected before any device work: exchange outside 0..3, lookahead > 32, the
     # pair schedule (lookahead 17..32) on several column parts
-    for field, value, extra in (("exchange", 3, {}), ("exchange", -1, {}), ("lookahead", 33, {}),
+    for field, value, extra in (("exchange", 4, {}), ("exchange", -1, {}), ("lookahead", 33, {}),
                                 ("lookahead", 32, {"virtual_ranks": 2})):
         o = sx.default_options()
         setattr(o, field, value)
@@ -140,3 +140,28 @@ def test_product_never_imports_the_oracle():
     assert includes and all(h in ("math.h", "stdint.h", "stdlib.h", "string.h") for h in includes)
     oracle_py = open(os.path.join(ROOT, "oracle", "__init__.py")).read()
     assert not re.search(r"^\s*(import|from)\s+paper_2211_10979_b200", oracle_py, flags=re.M)
+
+
+def test_product_library_reads_no_environment():
+    """Experiment hooks (SIMPLEX_* environment variables) are compiled only into the
+    -DSIMPLEX_EXPERIMENTS variant used by scripts/; the product .so has none of their names,
+    and the binding loads only the in-tree product library."""
+    data = open(sx.LIB_PATH, "rb").read()
+    for name in (b"SIMPLEX_PROBE", b"SIMPLEX_PASS_CFG", b"SIMPLEX_LOOK_CLUSTER", b"SIMPLEX_NO_PDL",
+                 b"SIMPLEX_NO_LOOK_CACHE", b"SIMPLEX_FORCE_NCCL", b"SIMPLEX_NO_MBLOCK", b"SIMPLEX_PASS_SMS",
+                 b"SIMPLEX_TIME_SELECT"):
+        assert name not in data, name
+    src = open(os.path.join(ROOT, "paper_2211_10979_b200", "__init__.py")).read()
+    assert "os.environ" not in src and "getenv" not in src
+    assert os.path.dirname(sx.LIB_PATH) == os.path.join(ROOT, "paper_2211_10979_b200")
+
+
+def test_binding_validates_buffers_before_the_call():
+    """Shape / dtype mismatches are caught in the binding (ValueError), never handed to the
+    C ABI as a short buffer (out-of-bounds reads in simplex_create)."""
+    A = np.ones((3, 4))
+    for b, c in ((np.ones(2), np.ones(4)), (np.ones(3), np.ones(5)), (np.ones((3, 1)), np.ones(4))):
+        with pytest.raises(ValueError):
+            sx.Simplex(A, b, c)
+    with pytest.raises(ValueError):
+        sx.Simplex(np.ones(3), np.ones(3), np.ones(3))

@@ -185,13 +185,12 @@ def test_multipart_peer_exchange_without_pipeline(sx, P, look):
 
 
 @pytest.mark.parametrize("P", [2, 5])
-def test_multipart_peer_exchange_per_pivot_launches(sx, P, monkeypatch):
-    """The peer-memory protocol with one k_mlook launch per pivot (SIMPLEX_NO_MBLOCK) instead of
+def test_multipart_peer_exchange_per_pivot_launches(sx, P):
+    """The peer-memory protocol with one k_mlook launch per pivot (exchange = 3) instead of
     one k_mblock per block (the virtual slabs then run in stream order, not concurrently)."""
-    monkeypatch.setenv("SIMPLEX_NO_MBLOCK", "1")
     A, b, c = lpgen.dense_lp(120, 200, 77)
     o = oracle.solve(A, b, c, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=16, exchange=2), o)
+    assert_same(gpu_solve(sx, A, b, c, virtual_ranks=P, lookahead=16, exchange=3), o)
 
 
 def test_multipart_peer_exchange_reset_and_options(sx):
@@ -243,12 +242,12 @@ def test_multipart_iterate_stepwise(sx, xch):
                 break
 
 
-def test_multipart_nccl_one_rank(sx, monkeypatch):
-    """k_mlook with the captured ncclAllGather of candidate columns, 1-rank communicator."""
-    monkeypatch.setenv("SIMPLEX_FORCE_NCCL", "1")
+def test_multipart_nccl_one_rank(sx):
+    """k_mlook with the captured ncclAllGather of candidate columns, 1-rank communicator
+    (exchange = 1 on one column part)."""
     A, b, c = lpgen.dense_lp(150, 230, 21)
     o = oracle.solve(A, b, c, keep_tableau=True)
-    assert_same(gpu_solve(sx, A, b, c, lookahead=16), o)
+    assert_same(gpu_solve(sx, A, b, c, lookahead=16, exchange=1), o)
 
 
 def test_multipart_golden_1000(sx):

@@ -257,13 +257,12 @@ def test_golden_full_size(sx, key):
     assert not cert.violations, cert.violations
 
 
-def test_nccl_exchange_path_one_rank(sx, monkeypatch):
+def test_nccl_exchange_path_one_rank(sx):
     """The multi-GPU exchange (k_pack -> ncclAllGather captured in the CUDA graph ->
     k_select from the gathered buffer) run through a real 1-rank NCCL communicator."""
     A, b, c = lpgen.dense_lp(150, 230, 21)
     o = oracle.solve(A, b, c, keep_tableau=True)
-    monkeypatch.setenv("SIMPLEX_FORCE_NCCL", "1")
-    g = gpu_solve(sx, A, b, c)
+    g = gpu_solve(sx, A, b, c, exchange=1)
     assert_same(g, o)
 
 
