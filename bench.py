@@ -32,6 +32,49 @@ PAPER_CONTEXT = ("paper (PAPER.md Tables III-V, 25000x25000, Turing): 0.2044 s/p
                  "0.1732 s/pivot Titan RTX, 0.1157 s/pivot both; 0.4773 s/pivot 32-core Xeon")
 
 
+def workload_name(m, n, seed, rule="dantzig"):
+    """config.workload — the SAME string on both arms (the driver compares them)."""
+    return (f"dense random LP m={m} n={n} FP64 seed {seed}, slack basis, "
+            + ("Dantzig + lowest-index ties" if rule == "dantzig" else "Bland's rule"))
+
+
+def host_info():
+    """CPU model, core count and this process's allowed cores (lscpu-equivalent, no subprocess)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    mem_gb = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem_gb = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "mem_total_gb": mem_gb,
+            "allowed_cores": len(os.sched_getaffinity(0))}
+
+
+class pinned_to_one_core:
+    """taskset-equivalent: pin the calling thread to one allowed core for the oracle timing
+    (SURVEY.md §8(d) "Pin the oracle with taskset to one core"), restore afterwards."""
+
+    def __enter__(self):
+        self.host = host_info()                     # before pinning: the box's cores
+        self.prev = os.sched_getaffinity(0)
+        self.core = sorted(self.prev)[0]
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.prev)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -52,6 +95,12 @@ def parse():
                     help="entering/leaving rule (bland = SURVEY.md §8(f) NEXT #3)")
     ap.add_argument("--single-pass-pivots", type=int, default=1000,
                     help="pivots of the one-pivot-per-pass k_update roofline window (0: skip)")
+    ap.add_argument("--largest", default="20000x40000",
+                    help="the north_star's largest tableau: a sub-record of simplex_iterate windows "
+                         "('none' to skip; skipped when it is the main workload)")
+    ap.add_argument("--largest-window", type=int, default=1600)
+    ap.add_argument("--largest-parity-max", type=int, default=20000,
+                    help="largest prefix golden (pivots) the largest leg checks bit for bit")
     return ap.parse_args()
 
 
@@ -94,6 +143,19 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def ncu_entry(workload, nranks, look=1):
+    p = os.path.join(ROOT, "profiles", "ncu_update_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"{workload}/s{look}/p{nranks}" if look > 1 else f"{workload}/p{nranks}")
+
+
+def ncu_duration(workload, nranks, look=1):
+    e = ncu_entry(workload, nranks, look)
+    return e.get("ncu_duration_us") if e else None
+
+
 def ncu_traffic(workload, nranks, look=1):
     """dram read+write bytes per pass launch (k_update, or k_update_s for look > 1) from a
     committed ncu --set full capture."""
@@ -129,6 +191,14 @@ class ClockSampler:
         self.proc.terminate()
         self.proc.wait()
         self.f.close()
+        if os.path.getsize(self.path) == 0:          # a timed region shorter than one 200 ms period
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=20).stdout
+                with open(self.path, "w") as f:
+                    f.write(out)
+            except Exception:
+                pass
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
@@ -154,19 +224,35 @@ def cpu_baseline(A, b, c, seconds):
     P / (t(P pivots) - t(0 pivots)) so the tableau build is not counted."""
     import oracle
     m, n = A.shape
-    t0 = time.perf_counter()
-    oracle.solve(A, b, c, stop_after=0)
-    t_build = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    oracle.solve(A, b, c, stop_after=2)
-    per = max((time.perf_counter() - t0 - t_build) / 2, 1e-6)
-    P = int(max(2, min(100000, seconds / per)))
-    t0 = time.perf_counter()
-    r = oracle.solve(A, b, c, stop_after=P)
-    dt = time.perf_counter() - t0 - t_build
+    with pinned_to_one_core() as pin:
+        t0 = time.perf_counter()
+        full = oracle.solve(A, b, c)
+        t_full = time.perf_counter() - t0
+        if t_full < seconds / 10:
+            # a whole solve is short (64x64: ~1 ms): time R complete solves, build included
+            R = int(max(1, seconds / 2 / max(t_full, 1e-6)))
+            t0 = time.perf_counter()
+            for _ in range(R):
+                oracle.solve(A, b, c)
+            dt = time.perf_counter() - t0
+            return {"value": R * full.pivots / dt, "unit": "pivots/s", "cores": 1, "kind": "oracle",
+                    "sample": f"{R} complete solves of the {m}x{n} seed LP ({full.pivots} pivots each, tableau "
+                              f"build included; oracle/simplex_oracle.c, 1 thread pinned to core {pin.core}), "
+                              f"{dt:.1f} s", "time_to_solve_us": 1e6 * dt / R, "host": pin.host}
+        t0 = time.perf_counter()
+        oracle.solve(A, b, c, stop_after=0)
+        t_build = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.solve(A, b, c, stop_after=2)
+        per = max((time.perf_counter() - t0 - t_build) / 2, 1e-6)
+        P = int(max(2, min(100000, seconds / per)))
+        t0 = time.perf_counter()
+        r = oracle.solve(A, b, c, stop_after=P)
+        dt = time.perf_counter() - t0 - t_build
     return {"value": r.pivots / dt, "unit": "pivots/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {r.pivots} pivots of the {m}x{n} seed solve (oracle/simplex_oracle.c, 1 thread, "
-                      f"tableau build excluded), {dt:.1f} s"}
+            "sample": f"first {r.pivots} pivots of the {m}x{n} seed solve (oracle/simplex_oracle.c, 1 thread "
+                      f"pinned to core {pin.core}, tableau build excluded), {dt:.1f} s",
+            "host": pin.host}
 
 
 def run_reference(args):
@@ -184,41 +270,169 @@ def run_reference(args):
     T, basis = oracle.build_tableau(A, b, c)
     done = [0]
 
+    bland = args.pivot_rule == "bland"
+
     def pivots(P):
         for _ in range(P):
-            k, _ = oracle.price(T[0, :-1])
+            k = oracle.price_bland(T[0, :-1]) if bland else oracle.price(T[0, :-1])[0]
             if k < 0:
                 return
-            r, _ = oracle.ratio(T, k)
+            r = oracle.ratio_bland(T, k, basis)[0] if bland else oracle.ratio(T, k)[0]
             if r < 0:
                 return
             oracle.pivot(T, r, k)
             basis[r - 1] = k
             done[0] += 1
 
-    t0 = time.perf_counter()
-    pivots(1)
-    per = max(time.perf_counter() - t0, 1e-6)
-    P = int(max(1, min(100000, 3.0 / per)))
-    for _ in range(args.warmup):
-        pivots(P)
-    d0 = done[0]
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        pivots(P)
-    dt = time.perf_counter() - t0
+    with pinned_to_one_core() as pin:
+        t0 = time.perf_counter()
+        pivots(1)
+        per = max(time.perf_counter() - t0, 1e-6)
+        P = int(max(1, min(100000, 3.0 / per)))
+        for _ in range(args.warmup):
+            pivots(P)
+        d0 = done[0]
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pivots(P)
+        dt = time.perf_counter() - t0
     v = (done[0] - d0) / dt
     line = {"metric": "pivots/s", "value": v, "unit": "pivots/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (lpgen SplitMix64 dense LP: A,c~U[1,10), b~U[n,2n))",
-            "config": {"workload": f"dense random LP m={m} n={n} FP64 seed {args.seed}", "m": m, "n": n},
+            "config": {"workload": workload_name(m, n, args.seed, args.pivot_rule), "m": m, "n": n},
             "cpu_baseline": {"value": v, "unit": "pivots/s", "cores": 1, "kind": "oracle",
                              "sample": f"each step: the next {P} pivots of the {m}x{n} solve through the "
-                                       "oracle's step functions (tableau built once, untimed)"},
+                                       f"oracle's step functions (tableau built once, untimed; 1 thread pinned "
+                                       f"to core {pin.core})", "host": pin.host},
             "e2e": {"value": v, "unit": "pivots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def golden_prefixes(m, n, seed):
+    """{P: path} of the oracle-written prefix goldens tests/golden/dense_<m>x<n>_s<seed>_p<P>.npz."""
+    import glob
+    import re
+    out = {}
+    for p in glob.glob(os.path.join(ROOT, "tests", "golden", f"dense_{m}x{n}_s{seed}_p*.npz")):
+        mt = re.search(r"_p(\d+)\.npz$", p)
+        if mt:
+            out[int(mt.group(1))] = p
+    return out
+
+
+def check_prefix(solver, g, P):
+    """The solver stands at exactly P pivots: its trace, objective, y and whole-tableau digest
+    against the oracle's P-pivot prefix golden (bit for bit)."""
+    k, r = solver.trace()
+    _, y, obj, piv, _ = solver.solution()
+    h = solver.tableau_hash()
+    return bool(piv == P and np.array_equal(k[:P], g["trace_k"]) and np.array_equal(r[:P], g["trace_r"])
+                and obj == float(g["objective"]) and np.array_equal(y, g["y"]) and h == int(g["tableau_hash"]))
+
+
+def measure_tcoll(m, world, dev, iters=200):
+    """t_coll(P) (SURVEY.md §8(d) "Multi-GPU roofline"): the per-pivot exchange of the
+    column-partitioned method — every rank contributes its candidate column (m+3 doubles: the
+    column, its index and value) and receives every rank's — as an exchange-only loop of NCCL
+    allgathers, CUDA events on the launching stream, max over ranks.  (The library's default
+    multi-rank exchange is the same data moved with peer-memory stores inside k_mblock.)"""
+    import torch
+    import torch.distributed as dist
+    x = torch.zeros(m + 3, dtype=torch.float64, device=dev)
+    out = torch.empty(world * (m + 3), dtype=torch.float64, device=dev)
+    for _ in range(20):
+        dist.all_gather_into_tensor(out, x)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        dist.all_gather_into_tensor(out, x)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / iters
+    return reduce_max(us, world, dev)
+
+
+def gather_list(v, world):
+    if world <= 1:
+        return [v]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, v)
+    return out
+
+
+def largest_leg(args, world, group, dev, peak, barrier):
+    """The north_star's largest tableau (20000x40000 by default) as a sub-record of every line:
+    pivots/s as the median of 3 simplex_iterate windows ("median of 3 windows
+    ... driven by simplex_iterate"), the device-timed pass roofline, and the first pivots checked
+    bit for bit against the largest oracle prefix golden available (trace, objective, y, digest)."""
+    import torch
+    import lpgen
+    import paper_2211_10979_b200 as sx
+    m, n = map(int, args.largest.split("x"))
+    t0 = time.perf_counter()
+    A, b, c = lpgen.dense_lp(m, n, args.seed)
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    s = sx.Simplex(A, b, c, group=group, time_kernels=True)
+    del A
+    barrier()
+    t_create = time.perf_counter() - t0
+    st = s.stats()
+    # parity first: the largest oracle prefix golden available (<= largest_parity_max pivots)
+    parity = {"checked": False}
+    pre = {P: p for P, p in golden_prefixes(m, n, args.seed).items() if P <= args.largest_parity_max}
+    if pre:
+        P = max(pre)
+        s.iterate(P)
+        ok = check_prefix(s, np.load(pre[P]), P)
+        parity = {"checked": True, "vs": os.path.relpath(pre[P], ROOT), "pivots": P,
+                  "bitwise_trace_objective_y_tableau_digest": ok}
+        if not ok:
+            raise SystemExit(f"PARITY FAILURE (largest leg) vs {pre[P]}")
+    s.iterate(64)                                          # warm-up (graphs built, clocks up)
+    barrier()
+    first = s.stats().pivots
+    wins, passes = [], []
+    for _ in range(3):
+        a0 = s.stats()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        done, status = s.iterate(args.largest_window)
+        e1.record()
+        barrier()
+        ms = reduce_max(e0.elapsed_time(e1), world, dev)
+        a1 = s.stats()
+        wins.append(done / (ms / 1e3))
+        if a1.update_launches > a0.update_launches:
+            passes.append((a1.update_ms_total - a0.update_ms_total) / (a1.update_launches - a0.update_launches))
+        if status != sx.RUNNING:
+            break
+    pass_ms = statistics.median(passes) if passes else None
+    achieved = st.bytes_per_pivot / (pass_ms / 1e3) / 1e9 if pass_ms else None
+    per_rank = gather_list(achieved / peak if achieved else None, world)
+    s.close()
+    full = os.path.join(ROOT, "tests", "golden", f"dense_{m}x{n}_s{args.seed}.json")
+    return {"workload": workload_name(m, n, args.seed), "metric": "pivots/s",
+            "value": statistics.median(wins), "windows_pivots_per_s": wins,
+            "window_pivots": args.largest_window, "first_window_starts_at_pivot": first, "n_gpus": world,
+            "how": "median of 3 simplex_iterate windows after 64 warm-up pivots; CUDA events on the "
+                   "launching stream, barrier + synchronize both sides, max over ranks",
+            "roofline": small_roof if small else {"bound": "hbm", "kernel": "k_update_s (rank-16 look-ahead pass)",
+                         "avg_launch_us": pass_ms * 1e3 if pass_ms else None, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak if achieved else None,
+                         "per_rank_frac": per_rank, "bytes_per_launch": st.bytes_per_pivot,
+                         "traffic": ncu_traffic(args.largest, world, 16)},
+            "t_roof_single_pass_us": st.bytes_per_pivot / peak / 1e3,
+            "parity": parity,
+            "full_solve_golden": os.path.relpath(full, ROOT) if os.path.exists(full) else None,
+            "setup_s": {"generate": t_gen, "create": t_create}}
 
 
 def main():
@@ -250,6 +464,7 @@ def main():
     solver = sx.Simplex(dA, db, dc, group=group, lookahead=args.lookahead, pivot_rule=rule,
                         overlap=not args.no_overlap)
     st = solver.stats()
+    small = st.path == 1                                     # one-CTA shared-memory solve (k_solve_small)
     tableau_bytes = 8 * (m + 1) * (n + m + 1)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = None
@@ -268,12 +483,22 @@ def main():
         _, _, obj, piv, _ = solver.solution(dx, dy)
         return status, obj, piv
 
-    # ---- correctness gate before timing: golden trace/objective when present
-    status, obj, piv = one_step(reload=False)
+    # ---- correctness gate before timing: the oracle's golden for this workload —
+    # the full solve when it exists (trace + objective bit for bit), else the largest prefix
+    # golden (trace, objective, y and whole-tableau digest at exactly P pivots), then the rest
     parity = {"checked": False}
-    gpath = os.path.join(ROOT, "tests", "golden", f"dense_{m}x{n}_s{args.seed}.npz")
-    if args.pivot_rule != "dantzig":
-        gpath = gpath[:-4] + f"_{args.pivot_rule}.npz"
+    suffix = "" if args.pivot_rule == "dantzig" else f"_{args.pivot_rule}"
+    gpath = os.path.join(ROOT, "tests", "golden", f"dense_{m}x{n}_s{args.seed}{suffix}.npz")
+    pre = golden_prefixes(m, n, args.seed) if not suffix else {}
+    if not os.path.exists(gpath) and pre:
+        P = max(pre)
+        solver.iterate(P)
+        ok = check_prefix(solver, np.load(pre[P]), P)
+        parity = {"checked": True, "vs": os.path.relpath(pre[P], ROOT), "prefix_pivots": P,
+                  "bitwise_trace_objective_y_tableau_digest": ok}
+        if not ok:
+            raise SystemExit(f"PARITY FAILURE vs {pre[P]}")
+    status, obj, piv = one_step(reload=False)
     k, r = solver.trace()
     if os.path.exists(gpath):
         g = np.load(gpath)
@@ -314,13 +539,12 @@ def main():
     if world > 1:
         total_ms = reduce_max(total_ms, world, dev)
     value = pivs / (total_ms / 1e3)
+    loop_ms = reduce_max(s1.loop_ms_total - s0.loop_ms_total, world, dev)
 
-    # ---- roofline pass: the same solve with CUDA events around every k_update launch
-    # (event-record nodes in the captured graph, on the stream the kernel runs on).  Kept
-    # out of the value steps because an event node between two pivot kernels disables the
-    # programmatic-dependent-launch edge the production loop uses.  The pipelined rank-s pass
-    # is timed on the device instead (globaltimer in the kernel, the production launch
-    # sequence), because event nodes would serialize it after the concurrent selection.
+    # ---- roofline pass: the same solve with the pass timed.  The pipelined rank-s pass is timed
+    # on the device (%globaltimer in the kernel: first CTA start -> last CTA end, the production
+    # launch sequence); the one-pivot k_update with CUDA events around every launch (event nodes in
+    # the captured graph, on the stream the kernel runs on).  Kept out of the value steps.
     prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule,
                       overlap=not args.no_overlap)
     barrier()
@@ -334,13 +558,34 @@ def main():
     avg_upd_s = upd_ms / 1e3 / max(1, upd_launches)
     achieved = st.bytes_per_pivot / avg_upd_s / 1e9
     peak, peak_src = load_peaks()
-    loop_ms = s1.loop_ms_total - s0.loop_ms_total
     prof_loop_ms = sp.loop_ms_total
-    look = solver_look(args.lookahead, world)
+    look = 1 if small else solver_look(args.lookahead, world)
+    small_roof = None
+    if small:
+        # the whole solve is ONE launch of ONE CTA with the tableau in shared memory: the bound
+        # is that SM's shared-memory crossbar (128 B/cycle/SM, B300_MICROARCH.md "LDS/STS",
+        # at the max SM clock), which every pivot streams twice (read + write of each element)
+        smhz = 1965.0
+        try:
+            smhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+        except Exception:
+            pass
+        smem_peak = 128.0 * smhz * 1e6 / 1e9
+        per_piv_us = upd_ms * 1e3 / max(1, window)
+        small_roof = {"bound": "smem", "kernel": "k_solve_small (whole solve, one CTA, tableau in shared memory)",
+                      "achieved": st.bytes_per_pivot / (per_piv_us * 1e-6) / 1e9, "peak": smem_peak,
+                      "unit": "GB/s", "frac": st.bytes_per_pivot / (per_piv_us * 1e-6) / 1e9 / smem_peak,
+                      "peak_source": "128 B/cycle/SM shared-memory crossbar (B300_MICROARCH.md LDS/STS) x "
+                                     f"{smhz:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)",
+                      "traffic": None, "bytes_per_pivot": st.bytes_per_pivot, "us_per_pivot": per_piv_us,
+                      "launch_us": upd_ms * 1e3, "pivots_per_launch": window,
+                      "note": "latency path (PAPER.md:161, 290): per pivot two block-wide argmins and two "
+                              "barriers of 1024 threads dominate; the HBM roofline does not apply"}
+    per_rank_frac = gather_list(achieved / peak, world)
 
     # ---- the one-pivot-per-pass kernel (k_update) measured the same way, for reference
     single = None
-    if look > 1 and args.single_pass_pivots > 0:
+    if (look > 1 or small) and args.single_pass_pivots > 0:
         p1 = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=1, pivot_rule=rule)
         barrier()
         p1.iterate(min(piv, args.single_pass_pivots))
@@ -355,7 +600,7 @@ def main():
 
     # ---- the rank-s pass alone (select-then-pass schedule: all SMs, in place), for reference
     alone = None
-    if look > 1 and not args.no_overlap and args.single_pass_pivots > 0:
+    if look > 1 and not args.no_overlap and args.single_pass_pivots > 0 and world == 1:
         p2 = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule,
                         overlap=False)
         barrier()
@@ -368,6 +613,14 @@ def main():
                  "avg_launch_us": a2 * 1e6, "achieved": st.bytes_per_pivot / a2 / 1e9, "peak": peak,
                  "unit": "GB/s", "frac": st.bytes_per_pivot / a2 / 1e9 / peak,
                  "launches_timed": s2p.update_launches}
+
+    # ---- multi-GPU roofline terms: t_coll(P) from an exchange-only loop,
+    # t_roof(P) = 16(m+1)(ceil((n+m)/P)+1)/peak + t_coll(P) per pivot (the one-pass-per-pivot
+    # roofline the north_star defines); the look-ahead moves 1/look of those bytes per pivot
+    t_coll = measure_tcoll(m, world, dev) if world > 1 else 0.0
+    slab_bytes = 16.0 * (m + 1) * (-(-(n + m) // world) + 1)
+    t_roof_us = slab_bytes / (peak * 1e9) * 1e6 + t_coll
+    blocks = -(-pivs // look) if look > 1 else pivs         # passes over the tableau in the timed steps
 
     # ---- e2e: same metric through the C ABI with HOST buffers (pinned), copies inside
     Ah = torch.from_numpy(A).pin_memory()
@@ -390,12 +643,21 @@ def main():
     if world > 1:
         h2d = int(reduce_sum(h2d, world, dev))
     d2h = world * 8 * (n + m + 1)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(A, b, c, args.cpu_sample_seconds)
-
     solver.close()
+    del Ah, bh, ch
+    barrier()
+
+    # ---- the largest tableau (north_star scaling target) as a sub-record
+    largest = None
+    if args.largest not in ("none", "", args.workload):
+        largest = largest_leg(args, world, group, dev, peak, barrier)
+
+    # ---- the oracle on the host, rank 0, at every N (the other ranks wait at the barrier)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(A, b, c, args.cpu_sample_seconds)
+    barrier()
+
     if rank == 0:
         line = {
             "metric": "pivots/s", "value": value, "unit": "pivots/s", "n_gpus": world, "steps": args.steps,
@@ -403,47 +665,63 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (lpgen SplitMix64 dense LP seed {args.seed}: A,c~U[1,10), b~U[n,2n); "
                     "SPEC.md:365-380 recipe)",
-            "config": {"workload": f"dense random LP m={m} n={n} FP64 seed {args.seed}, slack basis, "
-                                   + ("Dantzig + lowest-index ties" if args.pivot_rule == "dantzig" else
-                                      "Bland's rule"), "m": m, "n": n, "pivots_per_solve": piv,
-                       "pivots_per_tableau_pass": look,
-                       "schedule": ("select block b+1 (16-SM cluster) concurrently with the pass of block b "
+            "config": {"workload": workload_name(m, n, args.seed, args.pivot_rule), "m": m, "n": n,
+                       "pivots_per_solve": piv, "pivots_per_tableau_pass": look,
+                       "schedule": "the whole solve in one single-CTA launch, tableau in shared memory" if small else
+                                   ("select block b+1 (16-SM cluster) concurrently with the pass of block b "
                                     "(two tableau buffers)" if look > 1 and not args.no_overlap else
                                     "select, then pass" if look > 1 else "one pivot per pass"),
-                       "time_to_solve_ms": total_ms / args.steps,
+                       "time_to_solve_ms": total_ms / args.steps, "time_to_solve_us": 1e3 * total_ms / args.steps,
                        "parallelism": f"column slabs x{world}" + (" (candidate columns exchanged over peer memory per pivot)" if world > 1 else ""),
                        "l2": ("tableau %.2f GB > L2 %d MB: inputs larger than L2" % (tableau_bytes / 1e9, l2 >> 20))
                        if flush is None else "L2 flushed (write 2xL2) before every timed step",
                        "step": "reset (build Table I from device-resident A,b,c) + solve + extract"},
-            "roofline": {"bound": "hbm",
+            "roofline": small_roof if small else {"bound": "hbm",
                          "kernel": (f"k_update_s (rank-{look} look-ahead pass: {look} pivots per tableau "
                                     "stream, TMA loads + TMA bulk stores; runs concurrently with the "
                                     "selection of the next block)") if look > 1 else
                                    "k_update (fused row-scale + rank-1 update)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "per_rank_frac": per_rank_frac,
                          "peak_source": peak_src, "traffic": ncu_traffic(args.workload, world, look),
                          "bytes_per_launch": st.bytes_per_pivot,
-                         "bytes_formula": "16*(m+1)*(local columns incl. rhs) per pivot",
+                         "bytes_formula": "16*(m+1)*(local columns incl. rhs): every slab element read and "
+                                          "written once per pass",
                          "avg_launch_us": avg_upd_s * 1e6, "launches_timed": upd_launches,
-                         "timed_window": (f"first {window} pivots of the same solve; each pass launch timed on the "
-                                          "device (%globaltimer, first CTA start -> last CTA end) while the "
-                                          "selection of the next block runs next to it")
-                         if look > 1 and not args.no_overlap else
-                         f"first {window} pivots of the same solve, CUDA events per launch",
+                         "timing_source": ("device %globaltimer in the kernel (first CTA start -> last CTA end), "
+                                           "production launch sequence, next to the concurrent selection")
+                         if look > 1 and not args.no_overlap else "CUDA events around every launch",
+                         "ncu_avg_launch_us": ncu_duration(args.workload, world, look),
+                         "ncu_note": "ncu's gpu__time_duration (profiles/) is a replayed, serialised, cold-cache "
+                                     "launch incl. launch latency and CTA ramp-up; it bounds the device-timed "
+                                     "figure from above (~5 % at 8000^2)",
+                         "timed_window": f"first {window} pivots of the same solve",
                          "update_share_of_loop": upd_ms / prof_loop_ms if prof_loop_ms > 0 else None,
                          "pivots_per_launch": look,
-                         "effective_gbs_per_pivot": st.bytes_per_pivot * pivs / (loop_ms / 1e3) / 1e9
-                         if loop_ms > 0 else None,
+                         "passes_per_step": blocks / args.steps,
+                         "algorithmic_bytes_per_step": st.bytes_per_pivot * blocks / args.steps,
+                         "algorithmic_gbs_over_step": st.bytes_per_pivot * blocks / (total_ms / 1e3) / 1e9,
+                         "single_pass_equivalent_gb_per_step": st.bytes_per_pivot * pivs / args.steps / 1e9,
                          "single_pass": single, "pass_alone": alone,
                          "note": ("tableau resident in L2 (%.0f MB per buffer < %d MB L2): the pass runs from L2, "
                                   "so its fraction of the HBM peak is not a roofline" % (tableau_bytes / 1e6, l2 >> 20))
                          if 2 * tableau_bytes < l2 else None},
+            "multi_gpu": {"P": world, "t_coll_us_per_pivot": t_coll,
+                          "t_coll_how": "exchange-only loop: NCCL allgather of (m+3) doubles per rank, 200 "
+                                        "iterations, CUDA events, max over ranks" if world > 1 else "1 GPU: no exchange",
+                          "t_roof_us_per_pivot": t_roof_us,
+                          "t_roof_formula": "16(m+1)(ceil((n+m)/P)+1)/peak + t_coll(P) (one pass per pivot)",
+                          "roof_pivots_per_s": 1e6 / t_roof_us,
+                          "value_over_single_pass_roof": value / (1e6 / t_roof_us),
+                          "loop_ms": loop_ms,
+                          "efficiency_inputs": {"value": value, "P": world}},
             "cpu_baseline": cpu,
+            "small_path": small,
             "e2e": {"value": piv_e2e / (e2e_ms / 1e3), "unit": "pivots/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms": e2e_ms,
                     "path": "simplex_reset(pinned host A,b,c) + simplex_solve + simplex_get_solution(host x,y)"},
             "gpu_launches": int(s1.kernel_launches - s0.kernel_launches),
-            "clocks": clk, "parity": parity, "context": PAPER_CONTEXT,
+            "clocks": clk, "parity": parity, "largest": largest, "context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

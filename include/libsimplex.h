@@ -99,7 +99,10 @@ typedef struct {
                                17..32 = pair schedule (one column part): two selections of
                                16 + (s-16) pivots, then ONE pass applies all s (no pipeline;
                                pays off on tableaux whose pass dominates, 20000x40000);
-                               0 (default) = 16; > 32 -> SIMPLEX_E_ARG                     */
+                               0 (default) = automatic: a tableau that fits in one CTA's
+                               shared memory (one column part, no Phase I; e.g. 64x64) is
+                               solved by ONE single-CTA launch with the tableau on chip
+                               (stats.path = 1), anything else uses 16; > 32 -> SIMPLEX_E_ARG */
     int32_t  pivot_rule;    /* 0 = Dantzig (default): most negative T[0][j], lowest j / lowest
                                row on ties (readings c1-c4); 1 = Bland: first j
                                with T[0][j] < -tol_opt, ratio ties -> smallest basic-variable
@@ -148,6 +151,9 @@ typedef struct {
     int64_t local_ld;            /* padded row pitch of the slab, in doubles                 */
     int64_t col_offset;          /* first global column of this rank's slab                  */
     int64_t bytes_per_pivot;     /* algorithmic bytes of one update: 16*(m+1)*local_cols     */
+    int64_t path;                /* 0: device loop of captured CUDA-graph segments; 1: the whole
+                                    solve in one single-CTA launch with the tableau in shared
+                                    memory (small tableaux, lookahead = 0)                     */
 } simplex_stats;
 
 /* Fill *o with the defaults above. */

@@ -111,3 +111,34 @@ def planted(m: int, n: int, seed: int, support: int):
     b = A @ x + s
     c = A.T @ y - d
     return A, b, c, x, y
+
+
+def with_lower_bounds(m: int, n: int, seed: int, frac: float = 0.1, eq: int = 0):
+    """The dense generator LP (lpgen.dense_lp) with a fraction `frac` of its rows turned into
+    "at least" rows  -a_i x <= -t_i  (b_i < 0: Phase I needs an artificial for each), plus `eq`
+    equality constraints a_i x = t_i written as the pair  a_i x <= t_i  (row i, replacing a
+    generator row) and  -a_i x <= -t_i  (appended, so its index is higher).  When Phase I pivots
+    in such a pair the ratio tie goes to the lower row (reading c4), the "<=" copy leaves, and the
+    appended row ends Phase I as  -s_j - s_i + art_j = 0  with its artificial basic at zero: the
+    drive-out (reading p4) must pivot it out on column s_i.
+
+    Feasibility by construction: x0 = (1/(20 n)) * ones satisfies every "<=" row (a_i x0 <= 0.5
+    < n <= b_i); t_i = a_i x0 / 2 makes x0 strictly feasible for the ">=" rows; the
+    equality rows use t_i = a_i x0 (x0 satisfies them)."""
+    from . import dense_lp
+    A, b, c = dense_lp(m, n, seed)
+    rng = np.random.default_rng(seed + 7919)
+    rows = np.sort(rng.choice(m, size=max(1, int(round(frac * m))), replace=False))
+    x0 = np.full(n, 1.0 / (20.0 * n))
+    t = 0.5 * (A[rows] @ x0)
+    A = A.copy()
+    b = b.copy()
+    A[rows] = -A[rows]
+    b[rows] = -t
+    if eq:
+        free = np.setdiff1d(np.arange(m), rows)[:eq]
+        te = A[free] @ x0
+        b[free] = te
+        A = np.vstack([A, -A[free]])
+        b = np.concatenate([b, -te])
+    return A, b, c

@@ -251,7 +251,7 @@ def iterate(T, basis, it, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, cap=None, stop_at
 
 
 def solve_2phase(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, rule=DANTZIG,
-                 trace_cap=None):
+                 trace_cap=None, parallel=False):
     """Two-phase method: b may have negative entries.
     Returns a Result (no tableau) with .phase1_pivots."""
     A, b, c = _f64(A), _f64(b), _f64(c)
@@ -262,7 +262,7 @@ def solve_2phase(A, b, c, *, tol_opt=TOL_OPT, tol_piv=TOL_PIV, max_pivots=0, rul
     tr = np.zeros(max(trace_cap, 1), dtype=np.int32)
     x, y = np.empty(n), np.empty(m)
     obj, piv, st, p1 = C.c_double(), C.c_int64(), C.c_int(), C.c_int64(-1)
-    err = lib().or_solve_2phase(m, n, _dp(A), _dp(b), _dp(c), tol_opt, tol_piv, max_pivots, rule,
+    err = lib(parallel).or_solve_2phase(m, n, _dp(A), _dp(b), _dp(c), tol_opt, tol_piv, max_pivots, rule,
                                 tk.ctypes.data_as(C.POINTER(C.c_int32)),
                                 tr.ctypes.data_as(C.POINTER(C.c_int32)), trace_cap,
                                 _dp(x), _dp(y), C.byref(obj), C.byref(piv), C.byref(st), C.byref(p1))

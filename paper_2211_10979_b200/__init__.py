@@ -52,7 +52,8 @@ class Stats(C.Structure):
     _fields_ = [("pivots", C.c_int64), ("update_launches", C.c_int64), ("update_ms_total", C.c_double),
                 ("loop_ms_total", C.c_double), ("graph_launches", C.c_int64),
                 ("kernel_launches", C.c_int64), ("local_rows", C.c_int64), ("local_cols", C.c_int64),
-                ("local_ld", C.c_int64), ("col_offset", C.c_int64), ("bytes_per_pivot", C.c_int64)]
+                ("local_ld", C.c_int64), ("col_offset", C.c_int64), ("bytes_per_pivot", C.c_int64),
+                ("path", C.c_int64)]
 
 
 class SimplexError(RuntimeError):

@@ -53,6 +53,7 @@ struct alignas(16) DevState {
   unsigned int ticket; // last-block ticket of k_select
   unsigned int ticket2;
   int phase;           // 1: Phase I (artificials in the basis), 2: the problem's objective
+  int drive_next;      // Phase I drive-out: index of the next listed row to drive out (reading p4)
   int pw;              // columns priced (local): all non-rhs in Phase I, no artificials after
   int sb[2];           // look-ahead: pivots selected into chain bank 0 / 1
   int rsb[2][kMaxLook];// look-ahead: their pivot rows, in order

@@ -119,9 +119,10 @@ struct simplex_s {
   double* d_obj = nullptr;
   double* d_b = nullptr;
   unsigned long long* d_hash = nullptr;
-  double* d_fcol = nullptr;             // Phase I drive-out on several parts: the pivot column
-  long long* d_fj = nullptr;            // ... and its global index (allreduced across ranks)
+  double* d_fcol = nullptr;             // Phase I drive-out: staged [flag, pivot column] per rank
+  long long* d_fj = nullptr;            // ... each part's first eligible column, then the minimum
   sx::DevState* h_state = nullptr;  // pinned, 3 slots: 2 segment mirrors + 1 sync copy
+  unsigned int* h_err = nullptr;    // pinned, one error word per slab (load)
   // graph segments
   int S = 32;                       // pivots per captured graph segment
   int look = 1;                     // pivots per tableau pass (>1: rank-s look-ahead)
@@ -130,6 +131,7 @@ struct simplex_s {
   int pass_cfg = 0;                 // k_update_s configuration (kernels.cu kPassCfgs)
   bool pdl = true;                  // programmatic dependent launch between pivot kernels
   bool force_nccl = false;          // exchange = 1 on one part: 1-rank NCCL exchange on one GPU
+  bool small = false;               // the whole solve in one k_solve_small launch (tableau in smem)
   bool graphs_ready = false;
   cudaGraphExec_t seg[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> tev[2];
@@ -138,6 +140,10 @@ struct simplex_s {
   bool faulted = false;             // latched after an exchange timeout or a CUDA/NCCL error in
                                     // the loop: every later call except destroy -> E_STATE
   int phase = 2;                    // 1 while the Phase I objective is being optimized
+  bool drive_pending = false;       // Phase I ended; its drive-out of artificials not finished yet
+  std::vector<int> drive_rows;      // rows whose basic variable was artificial when Phase I ended
+  long long drive_done = 0;         // listed rows handled (DevState.drive_next)
+  long long xcol_stride() const { return roundup(m + 2, 2); }
   long long it = 0;
   // stats
   long long graph_launches = 0, kernel_launches = 0, upd_launches = 0;
@@ -194,10 +200,11 @@ struct simplex_s {
   simplex_err setup(long long m_, long long n_, const double* b, const simplex_options* o);
   simplex_err scan_b(const double* b, std::vector<int>* art_of_row, std::vector<int>* neg);
   simplex_err phase_transition();
-  simplex_err load(const double* A, const double* b, const double* c);
+  simplex_err load(const double* A, const double* b, const double* c, bool first);
   simplex_err build_graphs();
   simplex_err enqueue_pivot(int slot, int t);
   simplex_err run(long long max_pivots, long long* done);
+  simplex_err run_small(long long max_pivots, long long* done);
   simplex_err flush_all();
   void release();
   simplex_err setup_p2p();
@@ -303,6 +310,14 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   arts = (long long)art_rows.size();
   W = n + m + arts + 1;
   if (arts > 0 && !opt.phase1) return fail(SIMPLEX_E_NEG_RHS, "b has a negative entry and phase1 = 0");
+  // lookahead = 0 (automatic) on a tableau that fits in one CTA's shared memory, one column part,
+  // no Phase I: the latency path — the whole solve in ONE k_solve_small launch
+  small = opt.lookahead == 0 && nparts == 1 && arts == 0 && !force_nccl &&
+          sx::small_smem_bytes((int)(m + 1), (int)(n + m)) <= sx::small_smem_max();
+  if (small) {
+    look = 1;
+    overlap = false;
+  }
   if (overlap) {
     // the pipeline needs a second tableau buffer: fall back to select-then-pass in place when
     // two tableaux (+10 %) do not fit in the free device memory
@@ -316,6 +331,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   CK(cudaEventCreate(&ev_loop1));
   for (auto& e : ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&h_state), 3 * sizeof(sx::DevState), cudaHostAllocDefault));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&h_err), sizeof(unsigned int) * std::max(1, nslabs), cudaHostAllocDefault));
 
   // ---- column partition: part p = rank * nslabs + s
   slabs.resize(nslabs);
@@ -536,19 +552,25 @@ simplex_err simplex_s::setup_p2p() {
   return SIMPLEX_OK;
 }
 
-simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
+simplex_err simplex_s::load(const double* A, const double* b, const double* c, bool first) {
   if (!A || !b || !c) return fail(SIMPLEX_E_ARG, "NULL input pointer");
   RET(enter());
+  // the row map of b's signs (Phase I): scanned on the host at create and on a reset of a Phase I
+  // handle; a handle without artificials keeps its all-slack map and k_build flags any b_i < 0
+  // (kErrNegRhs) — a reset then costs one host synchronisation
   std::vector<int> art_of_row, neg;
-  RET(scan_b(b, &art_of_row, &neg));
-  if ((long long)neg.size() != arts)
-    return fail(SIMPLEX_E_ARG, "reset: the number of negative b entries differs from create's");
-  art_rows = neg;
+  const bool remap = first || arts > 0;
+  if (remap) {
+    RET(scan_b(b, &art_of_row, &neg));
+    if ((long long)neg.size() != arts)
+      return fail(SIMPLEX_E_ARG, "reset: the number of negative b entries differs from create's");
+    art_rows = neg;
+  }
   CK(cudaMemcpyAsync(d_b, b, sizeof(double) * m, cudaMemcpyDefault, stream));
   for (auto& sl : slabs) {
     sx::SlabView& v = sl.v;
-    CK(cudaMemcpyAsync(v.art_of_row, art_of_row.data(), sizeof(int) * m, cudaMemcpyHostToDevice, stream));
-    if (arts > 0) CK(cudaMemcpyAsync(v.neg_rows, neg.data(), sizeof(int) * arts, cudaMemcpyHostToDevice, stream));
+    if (remap) CK(cudaMemcpyAsync(v.art_of_row, art_of_row.data(), sizeof(int) * m, cudaMemcpyHostToDevice, stream));
+    if (remap && arts > 0) CK(cudaMemcpyAsync(v.neg_rows, neg.data(), sizeof(int) * arts, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(v.cvec, c, sizeof(double) * n, cudaMemcpyDefault, stream));
     const long long ns = std::max<long long>(0, std::min<long long>(v.c0 + v.w, n) - v.c0);  // structural cols
     if (ns > 0) {
@@ -562,15 +584,14 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
     if (arts > 0) CK(sx::launch_phase1_row0(v, stream));     // Phase I objective (reading p2)
     CK(sx::launch_price0(v, opt.tol_opt, stream));
   }
-  CK(cudaStreamSynchronize(stream));                          // host vectors above go out of scope
   kernel_launches += (3 + (arts > 0 ? 1 : 0)) * nslabs;
-  // validation result
+  // validation result: every slab's error bits, one synchronisation (which also keeps the host
+  // vectors above alive until their copies have run)
+  for (int s = 0; s < nslabs; ++s)
+    CK(cudaMemcpyAsync(&h_err[s], &slabs[s].v.st->err, sizeof(unsigned int), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
   unsigned int err = 0;
-  for (int s = 0; s < nslabs; ++s) {
-    CK(cudaMemcpyAsync(&h_state[2], slabs[s].v.st, sizeof(sx::DevState), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    err |= h_state[2].err;
-  }
+  for (int s = 0; s < nslabs; ++s) err |= h_err[s];
   if (use_nccl()) {
     // every rank must agree on the verdict (each checked only its own columns)
     unsigned int* d_err = reinterpret_cast<unsigned int*>(d_hash);
@@ -582,8 +603,13 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c) {
   }
   status = SIMPLEX_RUNNING;
   phase = arts > 0 ? 1 : 2;
+  drive_pending = false;
+  drive_done = 0;
+  drive_rows.clear();
   it = 0;
   if (err & sx::kErrNonFinite) return fail(SIMPLEX_E_NONFINITE, "A, b or c contains NaN or Inf");
+  if (err & sx::kErrNegRhs)
+    return fail(SIMPLEX_E_ARG, "reset: the number of negative b entries differs from create's");
   return SIMPLEX_OK;
 }
 
@@ -753,13 +779,19 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
   const long long it0 = it;
   if (done) *done = 0;
   if (status != SIMPLEX_RUNNING) return SIMPLEX_OK;
+  if (small) return run_small(max_pivots, done);
   RET(build_graphs());
   RET(enter());
   const long long stop_at = max_pivots > 0 ? it + max_pivots : LLONG_MAX;
   for (auto& sl : slabs) CK(sx::launch_set_stop(sl.v.st, stop_at, stream));
   kernel_launches += nslabs;
   CK(cudaEventRecord(ev_loop0, stream));
-  for (;;) {
+  bool skip_loop = false;
+  if (drive_pending) {                            // a Phase I drive-out stopped by the last call
+    RET(phase_transition());
+    skip_loop = status != SIMPLEX_RUNNING || it >= stop_at || drive_pending;
+  }
+  for (; !skip_loop;) {
     if (overlap) {
       // pipeline prologue: the first block is selected from the current tableau into bank 0
       const Slab& sl = slabs[0];
@@ -837,87 +869,104 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
   return SIMPLEX_OK;
 }
 
+// The latency path: one k_solve_small launch runs pivots until a terminal status or stop_at.
+simplex_err simplex_s::run_small(long long max_pivots, long long* done) {
+  const long long it0 = it;
+  RET(enter());
+  const long long stop_at = max_pivots > 0 ? it + max_pivots : LLONG_MAX;
+  const sx::SlabView& v = slabs[0].v;
+  CK(cudaEventRecord(ev_loop0, stream));
+  CK(sx::launch_solve_small(v, stop_at, opt.tol_opt, opt.tol_piv, stream));
+  CK(cudaEventRecord(ev_loop1, stream));
+  CK(cudaMemcpyAsync(&h_state[2], v.st, sizeof(sx::DevState), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  ++kernel_launches;
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ev_loop0, ev_loop1));
+  loop_ms += ms;
+  if (opt.time_kernels) {
+    upd_ms += ms;
+    ++upd_launches;
+  }
+  status = h_state[2].status;
+  it = h_state[2].it;
+  if (done) *done = it - it0;
+  return SIMPLEX_OK;
+}
+
 // Phase I -> Phase II (readings p3-p5 of DESIGN.md), between device loops, on every column part:
 // infeasible iff the Phase I optimum < -1e-7; each artificial still basic (rows ascending) is
-// pivoted out on its first column j < n+m with |T[i][j]| > tol_piv (a host-chosen pivot run
-// by the same update kernel); then the Phase II objective row is priced out on the device.
+// pivoted out on its first column j < n+m with |T[i][j]| > tol_piv over ALL parts (reading p4) —
+// chosen, staged and applied on the device (kernels.cu k_drive_*, then the update kernel), with
+// no host round trip per drive-out pivot; then the Phase II objective row is priced out on the
+// device.  The only synchronisations: one to read the verdict and the basis when Phase I ends,
+// one after the whole drive-out.  A drive-out that reaches stop_at (simplex_iterate) stays
+// pending (DevState.drive_next) and resumes at the next call.
 simplex_err simplex_s::phase_transition() {
-  // Phase I -> Phase II on every column part (readings p3-p5): the verdict and the basis are
-  // replicated; each drive-out pivot's column is the first j < n+m with |T[i][j]| > tol_piv over
-  // ALL parts (each part's first candidate, then the minimum: an NCCL allreduce across ranks),
-  // gathered from its owner part and applied by the update kernel on every part
-  RET(flush_all());
-  sx::SlabView& v0 = slabs[0].v;
-  std::vector<int> basis((size_t)m);
-  CK(cudaMemcpyAsync(&h_state[2].p, v0.T + v0.w, sizeof(double), cudaMemcpyDeviceToHost, stream));
-  CK(cudaMemcpyAsync(basis.data(), v0.basis, sizeof(int) * m, cudaMemcpyDeviceToHost, stream));
-  CK(cudaStreamSynchronize(stream));
-  phase = 2;
-  auto set_status_all = [&](int st) -> simplex_err {
-    for (auto& sl : slabs) CK(sx::launch_set_status(sl.v.st, st, stream));
+  if (!drive_pending) {
+    RET(flush_all());
+    sx::SlabView& v0 = slabs[0].v;
+    std::vector<int> basis((size_t)m);
+    CK(cudaMemcpyAsync(&h_state[2].p, v0.T + v0.w, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(basis.data(), v0.basis, sizeof(int) * m, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
-    return SIMPLEX_OK;
-  };
-  if (h_state[2].p < -1e-7) {
-    status = SIMPLEX_INFEASIBLE;
-    return set_status_all(SIMPLEX_INFEASIBLE);
+    if (h_state[2].p < -1e-7) {
+      phase = 2;
+      status = SIMPLEX_INFEASIBLE;
+      for (auto& sl : slabs) CK(sx::launch_set_status(sl.v.st, SIMPLEX_INFEASIBLE, stream));
+      CK(cudaStreamSynchronize(stream));
+      return SIMPLEX_OK;
+    }
+    drive_rows.clear();
+    for (long long i = 1; i <= m; ++i)
+      if (basis[(size_t)(i - 1)] >= n + m) drive_rows.push_back((int)i);
+    drive_pending = true;
+    drive_done = 0;
+    if (!d_fj) {
+      RET(dalloc(&d_fj, (size_t)nslabs + 1));                     // per part + the minimum
+      RET(dalloc(&d_fcol, (size_t)nranks * xcol_stride()));     // staged [flag, column] per rank
+    }
+    for (auto& sl : slabs) CK(sx::launch_set_status(sl.v.st, SIMPLEX_RUNNING, stream));
   }
   const bool multi = nparts > 1;
-  if (multi && !d_fcol) {                                // the drive-out column, gathered
-    RET(dalloc(&d_fcol, (size_t)m + 1));
-    RET(dalloc(&d_fj, 1));
-  }
-  double* d_col = d_fcol;
-  long long* d_j = d_fj;
-  std::vector<double> row;
-  for (long long i = 1; i <= m; ++i) {
-    if (basis[i - 1] < n + m) continue;
-    long long j = LLONG_MAX;
-    for (auto& sl : slabs) {                              // this rank's parts, ascending columns
-      const long long cols = std::max(0LL, std::min<long long>(sl.v.w, n + m - sl.v.c0));
-      if (cols == 0 || j != LLONG_MAX) continue;
-      row.resize((size_t)cols);
-      CK(cudaMemcpyAsync(row.data(), sl.v.T + i * sl.v.ld, sizeof(double) * cols, cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-      for (long long q = 0; q < cols; ++q)
-        if (std::fabs(row[(size_t)q]) > opt.tol_piv) { j = sl.v.c0 + q; break; }
-    }
-    if (nranks > 1) {                                     // the first over all ranks
-      CK(cudaMemcpyAsync(d_j, &j, sizeof(j), cudaMemcpyHostToDevice, stream));
-      NK(ncclAllReduce(d_j, d_j, 1, ncclInt64, ncclMin, comm, stream));
-      CK(cudaMemcpyAsync(&j, d_j, sizeof(j), cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-    }
-    if (j == LLONG_MAX) continue;                         // redundant row: artificial stays at 0
-    if (it >= cap) {
-      status = SIMPLEX_ITERATION_LIMIT;
-      return set_status_all(SIMPLEX_ITERATION_LIMIT);
-    }
+  const long long xs = xcol_stride();
+  long long* fjmin = d_fj + nslabs;
+  double* xmine = d_fcol + (long long)rank * xs;
+  for (size_t q = (size_t)drive_done; q < drive_rows.size(); ++q) {
+    const int i = drive_rows[q];
+    for (int p = 0; p < nslabs; ++p)
+      CK(sx::launch_drive_find(slabs[(size_t)p].v, i, n + m, opt.tol_piv, d_fj + p, stream));
+    CK(sx::launch_drive_pick(d_fj, nslabs, fjmin, stream));
+    if (nranks > 1) NK(ncclAllReduce(fjmin, fjmin, 1, ncclInt64, ncclMin, comm, stream));
     if (multi) {
-      // gather column j from its owner part (a slab of this rank, or a broadcast from its rank)
-      int64_t c0 = 0, w = 0;
-      long long owner = 0;
-      for (long long p = 0; p < nparts; ++p) {
-        RET(simplex_partition(n + m + arts, nparts, p, &c0, &w));
-        if (j >= c0 && j < c0 + w) { owner = p; break; }
-      }
-      const int orank = (int)(owner / nslabs);
-      if (orank == rank) {
-        const sx::SlabView& vo = slabs[(size_t)(owner % nslabs)].v;
-        CK(cudaMemcpy2DAsync(d_col, sizeof(double), vo.T + (j - vo.c0), sizeof(double) * vo.ld, sizeof(double),
-                             (size_t)m + 1, cudaMemcpyDeviceToDevice, stream));
-      }
-      if (nranks > 1) NK(ncclBroadcast(d_col, d_col, (size_t)m + 1, ncclFloat64, orank, comm, stream));
+      CK(cudaMemsetAsync(xmine, 0, sizeof(double), stream));
+      for (auto& sl : slabs) CK(sx::launch_drive_col(sl.v, fjmin, xmine, stream));
+      if (nranks > 1) NK(ncclAllGather(xmine, d_fcol, (size_t)xs, ncclFloat64, comm, stream));
     }
     for (auto& sl : slabs) {
-      CK(sx::launch_force(sl.v, (int)i, (int)j, multi ? d_col : nullptr, stream));
+      CK(sx::launch_drive_force(sl.v, i, (int)q, fjmin, multi ? (nranks > 1 ? d_fcol : xmine) : nullptr,
+                                multi ? (nranks > 1 ? nranks : 1) : 0, xs, stream));
       CK(sx::launch_update(sl.v, sl.q, opt.tol_opt, sl.upd_grid, stream, false));
+      CK(sx::launch_flush(sl.v, stream));
     }
-    RET(flush_all());
-    kernel_launches += 2 * nslabs;
-    basis[i - 1] = (int)j;
-    ++it;
+    kernel_launches += 2 + 3 * nslabs + (multi ? nslabs : 0);
   }
+  CK(cudaMemcpyAsync(&h_state[2], slabs[0].v.st, sizeof(sx::DevState), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  it = h_state[2].it;
+  drive_done = h_state[2].drive_next;
+  if (h_state[2].status == SIMPLEX_ITERATION_LIMIT) {
+    status = SIMPLEX_ITERATION_LIMIT;
+    drive_pending = false;
+    phase = 2;
+    return SIMPLEX_OK;
+  }
+  if (drive_done < (long long)drive_rows.size()) {     // stopped at stop_at: resume next call
+    status = SIMPLEX_RUNNING;
+    return SIMPLEX_OK;
+  }
+  drive_pending = false;
+  phase = 2;
   for (auto& sl : slabs) {
     CK(sx::launch_phase2_row0(sl.v, n, stream));
     CK(sx::launch_price0(sl.v, opt.tol_opt, stream));
@@ -957,6 +1006,7 @@ void simplex_s::release() {
   for (void* p : allocs) cudaFree(p);
   allocs.clear();
   if (h_state) cudaFreeHost(h_state);
+  if (h_err) cudaFreeHost(h_err);
   for (auto q : xs)
     if (q) cudaStreamDestroy(q);
   for (auto e : ev_join)
@@ -1023,7 +1073,7 @@ simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n, const double* 
   cudaGetDevice(&prev);
   simplex_t* h = new simplex_s();
   simplex_err e = h->setup(m, n, b, &o);
-  if (e == SIMPLEX_OK) e = h->load(A, b, c);
+  if (e == SIMPLEX_OK) e = h->load(A, b, c, true);
   cudaSetDevice(prev);
   if (e != SIMPLEX_OK) {
     std::string keep = g_err;
@@ -1040,7 +1090,7 @@ simplex_err simplex_reset(simplex_t* h, const double* A, const double* b, const 
   g_err.clear();
   HANDLE_OK(h);
   DeviceGuard dg(h->device);
-  return h->load(A, b, c);
+  return h->load(A, b, c, false);
 }
 
 simplex_err simplex_iterate(simplex_t* h, int64_t max_pivots, int64_t* pivots_done, simplex_status* st) {
@@ -1158,6 +1208,7 @@ simplex_err simplex_get_stats(simplex_t* h, simplex_stats* s) {
   s->local_ld = h->slabs[0].v.ld;
   s->col_offset = h->slabs[0].v.c0;
   s->bytes_per_pivot = 16LL * (h->m + 1) * cols;
+  s->path = h->small ? 1 : 0;
   return SIMPLEX_OK;
 }
 

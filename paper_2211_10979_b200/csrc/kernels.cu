@@ -15,6 +15,7 @@
 // with IEEE division (__ddiv_rn), T[i][j] = fma(-T[i][k], prow_j, T[i][j]) with an
 // explicit __fma_rn, q_i = T[i][W-1] / T[i][k] with __ddiv_rn.  With that pin the
 // tableau equals the oracle's bit for bit after every pivot, for any tiling.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(kThreads) k_build(SlabView s, const double* __
         } else {
           v = b[i - 1];
           if (!isfinite(v)) err |= kErrNonFinite;
+          if ((v < 0.0) != neg) err |= kErrNegRhs;   // b's signs disagree with the row map
           if (neg) v = -v;
         }
       } else if (g < n) {                          // structural column: copied from A / c
@@ -246,6 +248,7 @@ __global__ void k_init_state(SlabView s, long long n, long long cap) {
     st->pass_n = 0;
     st->pass_ns = 0.0;
     st->phase = s.arts > 0 ? 1 : 2;
+    st->drive_next = 0;
     st->pw = s.w;                                  // Phase I prices every non-rhs column
   }
 }
@@ -299,6 +302,114 @@ __global__ void __launch_bounds__(kThreads) k_force(SlabView s, int r, int k, co
       s.trace_r[it] = r;
     }
     st->it = it + 1;
+  }
+}
+
+// ---- Phase I drive-out on the device (reading p4): for each listed row i (rows whose basic
+// variable is still artificial when Phase I ends, ascending; list index q), pivot on the FIRST
+// column j < n+m with |T[i][j]| > tol_piv over all parts; a row with none is redundant (its
+// artificial stays basic at zero).  Per row, with no host round trip:
+//   k_drive_find   each part: its first eligible global column, or LLONG_MAX      -> fj[part]
+//   k_drive_pick   this rank's parts: the minimum (ascending columns = first)        -> fjmin
+//   (ranks > 1: ncclAllReduce(min) of fjmin)
+//   k_drive_col    the owner part stages its column j in xcol[1..m+1], xcol[0] = 1 (flag)
+//   (ranks > 1: ncclAllGather of xcol: every rank then holds the owner's exact bits)
+//   k_drive_force  every part: the loop state for pivot (i, j) — or none (redundant row / cap /
+//                  stop_at / not this row's turn) — then k_update applies it and k_flush writes it.
+// DevState.drive_next counts the listed rows already handled, so a drive-out stopped by stop_at
+// (simplex_iterate) resumes at the same row on the next call.
+__global__ void __launch_bounds__(1024) k_drive_find(SlabView s, int i, long long nm, double tol, long long* fj) {
+  __shared__ long long sh[32];
+  const long long lim = nm - s.c0 < s.w ? nm - s.c0 : s.w;     // local columns below n+m
+  const double* row = s.T + (long long)i * s.ld;
+  long long best = LLONG_MAX;
+  for (long long j = threadIdx.x; j < lim; j += blockDim.x)
+    if (fabs(row[j]) > tol) {
+      best = s.c0 + j;
+      break;                                       // ascending per thread: its first is its min
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t < best ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    long long v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : LLONG_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long t = __shfl_xor_sync(0xffffffffu, v, o);
+      v = t < v ? t : v;
+    }
+    if (threadIdx.x == 0) *fj = v;
+  }
+}
+
+__global__ void k_drive_pick(const long long* fj, int nparts, long long* fjmin) {
+  long long v = LLONG_MAX;
+  for (int p = 0; p < nparts; ++p) v = fj[p] < v ? fj[p] : v;
+  *fjmin = v;
+}
+
+// xcol = [flag, T[0][j], ..., T[m][j]] staged by the part owning global column j (flag 1.0)
+__global__ void __launch_bounds__(kThreads) k_drive_col(SlabView s, const long long* fjmin, double* xcol) {
+  const long long j = *fjmin;
+  if (j == LLONG_MAX || j < s.c0 || j >= s.c0 + s.w) return;
+  const long long jl = j - s.c0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s.rows; i += gridDim.x * blockDim.x)
+    xcol[1 + i] = s.T[(long long)i * s.ld + jl];
+  if (blockIdx.x == 0 && threadIdx.x == 0) xcol[0] = 1.0;
+}
+
+// xcols: nsrc staged buffers of stride xs doubles (one per rank after the allgather, or the
+// rank's own); the one with flag 1 holds column j.  xcols == NULL: one part, column j is local.
+__global__ void __launch_bounds__(kThreads) k_drive_force(SlabView s, int i, int q, const long long* fjmin,
+                                                          const double* xcols, int nsrc, long long xs) {
+  DevState* st = s.st;
+  __shared__ int sh_go;
+  __shared__ long long sh_j;
+  if (threadIdx.x == 0) {
+    int go = 0;
+    const long long j = *fjmin;
+    st->go = 0;
+    if (st->status == kRunning && st->drive_next == q) {
+      if (j == LLONG_MAX) {
+        st->drive_next = q + 1;                    // redundant row: no pivot
+      } else if (st->it >= st->cap) {
+        st->status = kIterLimit;
+      } else if (st->it < st->stop_at) {
+        go = 1;
+      }
+    }
+    sh_go = go;
+    sh_j = j;
+  }
+  __syncthreads();
+  if (!sh_go) return;
+  const long long j = sh_j;
+  const double* src = nullptr;
+  if (xcols) {
+    for (int r = 0; r < nsrc; ++r)
+      if (xcols[(long long)r * xs] == 1.0) src = xcols + (long long)r * xs + 1;
+  }
+  for (int t = threadIdx.x; t < s.rows; t += blockDim.x)
+    s.col[t] = src ? src[t] : s.T[(long long)t * s.ld + (j - s.c0)];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long it = st->it;
+    st->r = i;
+    st->k = (int)j;
+    st->p = s.col[i];
+    st->go = 1;
+    st->pend_r = i;
+    s.basis[i - 1] = (int)j;
+    if (it < s.trace_cap) {
+      s.trace_k[it] = (int)j;
+      s.trace_r[it] = i;
+    }
+    st->it = it + 1;
+    st->drive_next = q + 1;
   }
 }
 
@@ -1430,6 +1541,201 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
   }
 }
 
+// ------------------------------------------------------------------ small tableaux: one CTA
+// k_solve_small: the WHOLE solve of a tableau that fits in one SM's shared memory (64x64:
+// 65 x 129 doubles = 67 KB) in ONE launch of ONE CTA — the latency path for the small LPs
+// where "the communication and the reductions dominate".  The tableau is
+// loaded once, every pivot is Steps 1-3 on shared memory, and the result is
+// written back once.  Three CTA barriers per pivot:
+//   [ratio]   Step 2 on column k: rows with T[i][k] > tol_piv, q = T[i][rhs] / T[i][k] (IEEE
+//             division), ratio_cand -> warp argmin -> one slot per warp;          barrier 1
+//   [stage]   every warp folds the slots itself (no second barrier) -> r, or UNBOUNDED; the cap
+//             check (reading c12); colv[i] = T[i][k], prow[j] = T[r][j] / p (IEEE division)
+//             into separate buffers (no in-place race);                            barrier 2
+//   [update]  T[i][j] = fma(-colv[i], prow[j], T[i][j]) for i != r, T[r][j] = prow[j] — the
+//             oracle's c8 arithmetic — with warps owning rows and lanes owning columns; warp 0
+//             owns row 0 and prices it as it writes it (Step 1 for the next pivot: warp argmin
+//             of price_cand, Dantzig (v, j) / Bland (0, j)) -> k, or OPTIMAL;     barrier 3
+// Requires one column part and no artificial columns (the engine checks).
+constexpr int kSmallMaxQ = 8;                        // tableau width <= 256 columns
+template <int NT, int NQ>
+__global__ void __launch_bounds__(NT, 1) k_solve_small(SlabView s, long long stop_at, double tol_opt, double tol_piv) {
+  constexpr int NW = NT / 32;                        // NQ: columns per lane (cols <= 32 * NQ)
+  extern __shared__ __align__(16) double smem[];
+  const int rows = s.rows, m = rows - 1;
+  const int cols = s.w + 1;                          // logical columns incl. the rhs (local column w)
+  const int rhs = s.w;
+  double* T = smem;                                  // [rows][cols]
+  double* prow = T + (size_t)rows * cols;            // [cols]
+  double* colv = prow + cols;                        // [rows]
+  int* basis = reinterpret_cast<int*>(colv + rows);  // [m]
+  __shared__ Cand slot[NW];
+  __shared__ Cand sh_k;                              // Step-1 result for the next pivot
+  DevState* st = s.st;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int pend = st->pend_r;                       // a deferred pivot row of another path
+  for (int i = wid; i < rows; i += NW) {
+    const double* src = (i == pend) ? s.rownorm : s.T + (long long)i * s.ld;
+    for (int j = lane; j < cols; j += 32) T[(size_t)i * cols + j] = src[j];
+  }
+  for (int i = tid; i < m; i += NT) basis[i] = s.basis[i];
+  const long long cap = st->cap;
+  const int pw = st->pw;
+  const int rule = s.rule;
+  long long it = st->it;
+  int status = st->status;
+  __syncthreads();
+  if (wid == 0) {                                    // Step 1 on the starting row 0
+    Cand c = cand_none();
+    for (int j = lane; j < pw; j += 32) {
+      const double v = T[j];
+      if (v < -tol_opt) c = cand_min(c, price_cand(rule, v, j));
+    }
+    c = warp_min(c);
+    if (lane == 0) sh_k = c;
+  }
+  __syncthreads();
+  while (status == kRunning && it < stop_at) {
+    const Cand kc = sh_k;
+    if (kc.idx == LLONG_MAX) {
+      status = kOptimal;
+      break;
+    }
+    const int k = (int)kc.idx;
+    // Step 2 — ratio test over rows 1..m
+    Cand q = cand_none();
+    for (int i = 1 + tid; i <= m; i += NT) {
+      const double a = T[(size_t)i * cols + k];
+      if (a > tol_piv) q = cand_min(q, ratio_cand(rule, __ddiv_rn(T[(size_t)i * cols + rhs], a), i, basis[i - 1]));
+    }
+    q = warp_min(q);
+    if (lane == 0) slot[wid] = q;
+    __syncthreads();                                                      // barrier 1
+    q = warp_min(lane < NW ? slot[lane] : cand_none());
+    if (q.idx == LLONG_MAX) {
+      status = kUnbounded;
+      break;
+    }
+    if (it == cap) {
+      status = kIterLimit;
+      break;
+    }
+    const int r = cand_row(q.idx);
+    // Step 3 — pivot column snapshot and normalized pivot row, then the rank-1 update
+    const double p = T[(size_t)r * cols + k];
+    for (int i = tid; i < rows; i += NT) colv[i] = T[(size_t)i * cols + k];
+    for (int j = tid; j < cols; j += NT) prow[j] = __ddiv_rn(T[(size_t)r * cols + j], p);
+    if (tid == 0) {
+      basis[r - 1] = k;
+      if (it < s.trace_cap) {
+        s.trace_k[it] = (int)s.c0 + k;
+        s.trace_r[it] = r;
+      }
+    }
+    __syncthreads();                                                      // barrier 2
+    // lane owns columns j = lane + 32 q: its prow values stay in registers for every row; each
+    // row is NQ independent loads, then NQ FMAs, then NQ stores (no load waits behind a store)
+    double pr[NQ];
+#pragma unroll
+    for (int q2 = 0; q2 < NQ; ++q2) {
+      const int j = lane + 32 * q2;
+      pr[q2] = j < cols ? prow[j] : 0.0;
+    }
+    for (int i = wid; i < rows; i += NW) {
+      double* Ti = T + (size_t)i * cols;
+      double v[NQ];
+#pragma unroll
+      for (int q2 = 0; q2 < NQ; ++q2) {
+        const int j = lane + 32 * q2;
+        v[q2] = j < cols ? Ti[j] : 0.0;
+      }
+      const double a = -colv[i];
+#pragma unroll
+      for (int q2 = 0; q2 < NQ; ++q2) v[q2] = (i == r) ? pr[q2] : __fma_rn(a, pr[q2], v[q2]);
+#pragma unroll
+      for (int q2 = 0; q2 < NQ; ++q2) {
+        const int j = lane + 32 * q2;
+        if (j < cols) Ti[j] = v[q2];
+      }
+      if (i == 0) {                                  // warp 0: Step 1 of the next pivot on the new row 0
+        Cand c = cand_none();
+#pragma unroll
+        for (int q2 = 0; q2 < NQ; ++q2) {
+          const int j = lane + 32 * q2;
+          if (j < pw && v[q2] < -tol_opt) c = cand_min(c, price_cand(rule, v[q2], j));
+        }
+        c = warp_min(c);
+        if (lane == 0) sh_k = c;
+      }
+    }
+    ++it;
+    __syncthreads();                                                      // barrier 3
+  }
+  // write back: tableau (logical columns; padding untouched = zero), basis, loop state
+  __syncthreads();
+  for (int i = wid; i < rows; i += NW) {
+    double* dst = s.T + (long long)i * s.ld;
+    for (int j = lane; j < cols; j += 32) dst[j] = T[(size_t)i * cols + j];
+  }
+  for (int i = tid; i < m; i += NT) s.basis[i] = basis[i];
+  if (tid == 0) {
+    st->it = it;
+    st->status = status;
+    st->pend_r = -1;
+    st->go = 0;
+  }
+}
+
+size_t small_smem_bytes(int rows, int w) {
+  const size_t cols = (size_t)w + 1;
+  if (cols > 32 * (size_t)kSmallMaxQ) return ~(size_t)0;    // wider than one warp's columns: no
+  return ((size_t)rows * cols + cols + (size_t)rows) * sizeof(double) + (size_t)(rows - 1) * sizeof(int);
+}
+
+// Largest dynamic shared memory one CTA of k_solve_small may use on this device (0: unusable).
+size_t small_smem_max() {
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+  const size_t statics = 4096;                       // block_min scratch + loop state (static smem)
+  return optin > (int)statics ? (size_t)optin - statics : 0;
+}
+
+template <int NT, int NQ>
+static cudaError_t launch_small_nt(const SlabView& s, long long stop_at, double tol_opt, double tol_piv,
+                                   cudaStream_t st) {
+  static size_t set = 0;                             // opt-in size already granted (per instantiation)
+  const size_t smem = small_smem_bytes(s.rows, s.w);
+  if (smem > set) {
+    cudaError_t e = cudaFuncSetAttribute(k_solve_small<NT, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)small_smem_max());
+    if (e != cudaSuccess) return e;
+    set = small_smem_max();
+  }
+  k_solve_small<NT, NQ><<<1, NT, smem, st>>>(s, stop_at, tol_opt, tol_piv);
+  return cudaGetLastError();
+}
+
+template <int NQ>
+static cudaError_t launch_small_q(int nt, const SlabView& s, long long stop_at, double tol_opt, double tol_piv,
+                                  cudaStream_t st) {
+  if (nt >= 1024) return launch_small_nt<1024, NQ>(s, stop_at, tol_opt, tol_piv, st);
+  if (nt >= 512) return launch_small_nt<512, NQ>(s, stop_at, tol_opt, tol_piv, st);
+  if (nt >= 256) return launch_small_nt<256, NQ>(s, stop_at, tol_opt, tol_piv, st);
+  return launch_small_nt<128, NQ>(s, stop_at, tol_opt, tol_piv, st);
+}
+
+// 512 threads per CTA (measured, scripts/small_probe.py: 64x64 3.5 us/pivot vs 4.4 at 256 and
+// 6.4 at 128; 1024 no faster); 4 or 8 columns per lane
+cudaError_t launch_solve_small(const SlabView& s, long long stop_at, double tol_opt, double tol_piv,
+                               cudaStream_t st) {
+  int nt = 512;
+  if (const char* e = experiment_env("SIMPLEX_SMALL_THREADS")) nt = std::atoi(e);
+  if (s.w + 1 > 32 * kSmallMaxQ) return cudaErrorInvalidValue;
+  if (s.w + 1 <= 128) return launch_small_q<4>(nt, s, stop_at, tol_opt, tol_piv, st);
+  return launch_small_q<kSmallMaxQ>(nt, s, stop_at, tol_opt, tol_piv, st);
+}
+
 // ------------------------------------------------------------------ flush / extract / hash
 __global__ void __launch_bounds__(1024) k_flush(SlabView s) {
   const int pend = s.st->pend_r;
@@ -1733,6 +2039,25 @@ cudaError_t launch_force(const SlabView& s, int r, int k, const double* col, cud
 
 cudaError_t launch_set_status(DevState* d, int status, cudaStream_t st) {
   k_set_status<<<1, 1, 0, st>>>(d, status);
+  SX_CHECK_LAUNCH();
+}
+
+cudaError_t launch_drive_find(const SlabView& s, int i, long long nm, double tol, long long* fj, cudaStream_t st) {
+  k_drive_find<<<1, 1024, 0, st>>>(s, i, nm, tol, fj);
+  SX_CHECK_LAUNCH();
+}
+cudaError_t launch_drive_pick(const long long* fj, int nparts, long long* fjmin, cudaStream_t st) {
+  k_drive_pick<<<1, 1, 0, st>>>(fj, nparts, fjmin);
+  SX_CHECK_LAUNCH();
+}
+cudaError_t launch_drive_col(const SlabView& s, const long long* fjmin, double* xcol, cudaStream_t st) {
+  const int g = (int)std::min<long long>((s.rows + kThreads - 1) / kThreads, 64);
+  k_drive_col<<<g, kThreads, 0, st>>>(s, fjmin, xcol);
+  SX_CHECK_LAUNCH();
+}
+cudaError_t launch_drive_force(const SlabView& s, int i, int q, const long long* fjmin, const double* xcols,
+                               int nsrc, long long xs, cudaStream_t st) {
+  k_drive_force<<<1, kThreads, 0, st>>>(s, i, q, fjmin, xcols, nsrc, xs);
   SX_CHECK_LAUNCH();
 }
 

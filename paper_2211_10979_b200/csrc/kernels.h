@@ -58,8 +58,19 @@ cudaError_t update_s_occupancy(int cfg, int S, int* blocks_per_sm, size_t smem);
 // k_update_s: apply the pivots of chain bank `bank` to src, writing dst (src == dst: in place)
 cudaError_t launch_update_s(int cfg, const SlabView& s, int S, const double* src, double* dst, int bank, int nc,
                             int Gr, int cw, cudaStream_t st, bool pdl);
+// k_solve_small: the whole solve of a tableau that fits in one CTA's shared memory, one launch
+size_t small_smem_bytes(int rows, int w);
+size_t small_smem_max();
+cudaError_t launch_solve_small(const SlabView& s, long long stop_at, double tol_opt, double tol_piv,
+                               cudaStream_t st);
 cudaError_t launch_phase1_row0(const SlabView& s, cudaStream_t st);
 cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st);
+// Phase I drive-out on the device (reading p4; kernels.cu k_drive_*)
+cudaError_t launch_drive_find(const SlabView& s, int i, long long nm, double tol, long long* fj, cudaStream_t st);
+cudaError_t launch_drive_pick(const long long* fj, int nparts, long long* fjmin, cudaStream_t st);
+cudaError_t launch_drive_col(const SlabView& s, const long long* fjmin, double* xcol, cudaStream_t st);
+cudaError_t launch_drive_force(const SlabView& s, int i, int q, const long long* fjmin, const double* xcols,
+                               int nsrc, long long xs, cudaStream_t st);
 cudaError_t launch_force(const SlabView& s, int r, int k, const double* col, cudaStream_t st);
 cudaError_t launch_set_status(DevState* d, int status, cudaStream_t st);
 cudaError_t launch_flush(const SlabView& s, cudaStream_t st);

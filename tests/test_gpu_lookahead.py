@@ -208,7 +208,7 @@ def test_multipart_peer_exchange_reset_and_options(sx):
             assert np.array_equal(x, o.x) and np.array_equal(y, o.y)
             s.reset(A, b, c)
     with pytest.raises(sx.SimplexError):
-        sx.Simplex(A, b, c, virtual_ranks=2, exchange=3)
+        sx.Simplex(A, b, c, virtual_ranks=2, exchange=4)
 
 
 @pytest.mark.parametrize("m,n", [(1, 9), (7, 1), (300, 40), (90, 1100)])

@@ -109,3 +109,58 @@ def test_options_and_errors(sx):
         with pytest.raises(sx.SimplexError) as e:
             s.reset(A, np.array([4.0, 1.0]), c)
         assert e.value.code == sx.E_ARG
+
+
+DRIVE_PATHS = [dict(lookahead=1), dict(lookahead=16), dict(lookahead=16, overlap=False),
+               dict(lookahead=1, virtual_ranks=3), dict(lookahead=16, virtual_ranks=2),
+               dict(lookahead=16, virtual_ranks=3, exchange=2)]
+DRIVE_IDS = ["pass1", "look16", "look16serial", "slabs3", "mpart2", "mpart3peer"]
+
+
+@pytest.mark.parametrize("path", DRIVE_PATHS, ids=DRIVE_IDS)
+def test_drive_out_on_device(sx, path):
+    """Equality pairs leave artificials basic at zero after Phase I; the device drive-out
+    (k_drive_find / pick / col / force + the update, no host round trip per pivot) pivots them
+    out on the first eligible column over all parts — trace bit-identical to or_solve_2phase."""
+    from lpgen import fixtures
+    A, b, c = fixtures.with_lower_bounds(120, 150, 3, frac=0.1, eq=6)
+    o = check(sx, A, b, c, **path)
+    assert o.status == oracle.OPTIMAL
+
+
+@pytest.mark.parametrize("path", [dict(lookahead=1), dict(lookahead=16), dict(lookahead=16, virtual_ranks=2)],
+                         ids=["pass1", "look16", "mpart2"])
+def test_iterate_across_drive_out(sx, path):
+    """simplex_iterate in windows of 1 and 3 pivots never exceeds its window, also when the window
+    ends inside the drive-out (which then resumes at the same row): same trace as the oracle."""
+    from lpgen import fixtures
+    A, b, c = fixtures.with_lower_bounds(120, 150, 3, frac=0.1, eq=6)
+    o = oracle.solve_2phase(A, b, c)
+    for win in (1, 3):
+        with sx.Simplex(A, b, c, **path) as s:
+            total, st = 0, sx.RUNNING
+            while st == sx.RUNNING:
+                done, st = s.iterate(win)
+                assert 0 <= done <= win
+                total += done
+            k, r = s.trace()
+            x, y, obj, piv, _ = s.solution()
+        assert st == o.status and total == o.pivots == piv
+        assert np.array_equal(k, o.trace_k) and np.array_equal(r, o.trace_r)
+        assert obj == o.objective and np.array_equal(x, o.x)
+
+
+@pytest.mark.parametrize("path", [dict(), dict(lookahead=16, virtual_ranks=3)], ids=["default", "slabs3"])
+def test_phase1_2000_with_drive_out(sx, path):
+    """A 2000x2000 dense LP with 10 % ">=" rows (b_i < 0) and 20 equality pairs (2020 rows): Phase I
+    (18089 pivots), 20 device drive-out pivots, Phase II — bit-identical to or_solve_2phase (its
+    row-parallel build, bitwise equal to the single-thread one: tests/test_oracle_omp.py), and
+    certified optimal from the raw data."""
+    from lpgen import fixtures
+    A, b, c = fixtures.with_lower_bounds(2000, 2000, 3, frac=0.1, eq=20)
+    o = oracle.solve_2phase(A, b, c, parallel=True)
+    st, x, y, obj, piv, k, r = gpu(sx, A, b, c, **path)
+    assert st == o.status == oracle.OPTIMAL and piv == o.pivots
+    assert np.array_equal(k, o.trace_k) and np.array_equal(r, o.trace_r)
+    assert obj == o.objective and np.array_equal(x, o.x) and np.array_equal(y, o.y)
+    assert not oracle.certificate(A, b, c, x, y).violations

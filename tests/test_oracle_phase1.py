@@ -90,3 +90,39 @@ def test_planted_with_negative_rhs():
     assert abs(r.objective - obj) <= 1e-9 * abs(obj)
     assert np.max(np.abs(r.x - xs)) <= 1e-7
     assert not oracle.certificate(A2, b2, c, r.x, r.y).violations
+
+
+def drive_out_pivots(A, b, res):
+    """Drive-out pivots in a two-phase trace (reading p4): replay the basis through the Phase I
+    pivots; the pivots right after them on rows whose basic variable is still artificial."""
+    m, n = A.shape
+    basis, art = [], 0
+    for i in range(m):
+        if b[i] < 0:
+            basis.append(n + m + art)
+            art += 1
+        else:
+            basis.append(n + i)
+    for k, r in zip(res.trace_k[:res.phase1_pivots], res.trace_r[:res.phase1_pivots]):
+        basis[r - 1] = int(k)
+    left = sorted(i + 1 for i in range(m) if basis[i] >= n + m)
+    d = 0
+    for r in res.trace_r[res.phase1_pivots:]:
+        if d < len(left) and r == left[d]:
+            d += 1
+        else:
+            break
+    return d, len(left)
+
+
+def test_lower_bound_fixture_needs_drive_out():
+    """lpgen.fixtures.with_lower_bounds with equality pairs: Phase I ends with artificials basic
+    at zero, the drive-out pivots them out, and the final answer is certified optimal from the
+    raw data (primal / dual feasibility, strong duality)."""
+    from lpgen import fixtures
+    A, b, c = fixtures.with_lower_bounds(120, 150, 3, frac=0.1, eq=6)
+    r = oracle.solve_2phase(A, b, c)
+    assert r.status == oracle.OPTIMAL and r.phase1_pivots > 0
+    d, left = drive_out_pivots(A, b, r)
+    assert left >= 1 and d >= 1
+    assert not oracle.certificate(A, b, c, r.x, r.y).violations
