@@ -137,6 +137,14 @@ typedef struct {
                                returns SIMPLEX_E_NCCL and latches the handle (every later call
                                except destroy returns SIMPLEX_E_STATE).  Raise it when ranks may
                                launch far apart (e.g. under a profiler's kernel replay).    */
+    double   host_share;    /* hybrid CPU lane: the share
+                               θ in [0, 1) of the n+m columns kept in host memory and updated by
+                               the host cores (the LAST round(θ(n+m)) columns; at least one column
+                               stays on the GPU).  0 (default): off.  > 0 requires one GPU rank, no
+                               virtual ranks, lookahead 0 or 1 (one pivot per pass: the lanes
+                               exchange candidates every pivot), b >= 0; else SIMPLEX_E_ARG.
+                               Bitwise identical results.                                  */
+    int32_t  host_threads;  /* host threads of the CPU lane (<= 0: OpenMP's default)         */
 } simplex_options;
 
 typedef struct {
@@ -153,7 +161,10 @@ typedef struct {
     int64_t bytes_per_pivot;     /* algorithmic bytes of one update: 16*(m+1)*local_cols     */
     int64_t path;                /* 0: device loop of captured CUDA-graph segments; 1: the whole
                                     solve in one single-CTA launch with the tableau in shared
-                                    memory (small tableaux, lookahead = 0)                     */
+                                    memory (small tableaux, lookahead = 0); 2: hybrid CPU lane  */
+    int64_t host_cols;           /* columns of the hybrid CPU lane (0: none)                  */
+    double  host_ms_total;       /* host time spent updating the CPU lane's columns           */
+    double  host_wait_ms_total;  /* host time spent waiting for the GPU's candidate per pivot */
 } simplex_stats;
 
 /* Fill *o with the defaults above. */
@@ -179,16 +190,26 @@ simplex_err simplex_reset(simplex_t* h, const double* A, const double* b, const 
 simplex_err simplex_iterate(simplex_t* h, int64_t max_pivots, int64_t* pivots_done,
                             simplex_status* st);
 
-/* Iterate to termination (OPTIMAL, UNBOUNDED or ITERATION_LIMIT). */
+/* Iterate to termination: "repeat steps 1-3 till finding the best solution or the problem is
+ * proved to be unbounded" (§III Iterate/Finalization), with the iteration cap and
+ * the status precedence of DESIGN.md reading c12.  *st (may be NULL)
+ * receives OPTIMAL, UNBOUNDED, INFEASIBLE (Phase I) or ITERATION_LIMIT.  Same errors as
+ * simplex_iterate; on several ranks every rank must call it (collective). */
 simplex_err simplex_solve(simplex_t* h, simplex_status* st);
 
-/* x: n values (x_j = rhs of the row where j is basic, else 0), y: m dual values
- * (y_i = T[0][n+i-1]), objective = T[0][W-1]; any output pointer may be NULL.
- * Valid in any state (reports the current basis).  Multi-GPU: collective. */
+/* Read the solution off the current tableau (the objective is Table I's Z entry,
+ * PAPER.md:79-84): x: n values (x_j = rhs of the row where j is basic, else 0), y: m dual values
+ * (y_i = T[0][n+i-1], the slacks' reduced costs), objective = T[0][W-1], pivots done, status.
+ * Every output pointer may be NULL; x / y are caller-owned buffers of n / m doubles in host or
+ * device memory.  Valid in any state (reports the current basis).  Errors: ARG (NULL handle),
+ * STATE (faulted handle), CUDA.  Multi-GPU: collective (y is assembled from every rank). */
 simplex_err simplex_get_solution(simplex_t* h, double* x, double* y, double* objective,
                                  int64_t* pivots, simplex_status* st);
 
-/* Copy up to cap (k, r) pivot records into k[], r[] (host or device); *len = count. */
+/* The pivot trace (SPEC.md:195-198 PivotRecord; reading c19): copy up to cap (k, r) records —
+ * k the 0-based entering column, r the 1-based leaving row, in pivot order — into the caller's
+ * int32 buffers k[], r[] (host or device, cap entries each); *len = records copied.  Recorded only
+ * with options.record_trace = 1.  Errors: ARG (NULL handle, NULL buffer with cap > 0), STATE, CUDA. */
 simplex_err simplex_get_trace(simplex_t* h, int32_t* k, int32_t* r, int64_t cap, int64_t* len);
 
 /* Copy this rank's slab of the current tableau, logical columns only
@@ -206,7 +227,9 @@ simplex_err simplex_tableau_hash(simplex_t* h, uint64_t* hash);
 /* Counters and timings of the handle (see simplex_stats). */
 simplex_err simplex_get_stats(simplex_t* h, simplex_stats* s);
 
-/* Free everything the handle owns (NULL-safe). */
+/* Free everything the handle owns: device memory, streams, CUDA graphs, the NCCL communicator
+ * and peer mappings (the ownership rule of SURVEY.md §8(b)).  NULL-safe; valid on a faulted
+ * handle; always returns SIMPLEX_OK.  Multi-GPU: every rank destroys its own handle. */
 simplex_err simplex_destroy(simplex_t* h);
 
 /* Text of the last error on this thread ("" if none). */

@@ -45,7 +45,8 @@ class Options(C.Structure):
                 ("stream", C.c_void_p), ("virtual_ranks", C.c_int32), ("segment_pivots", C.c_int32),
                 ("time_kernels", C.c_int32), ("lookahead", C.c_int32),
                 ("pivot_rule", C.c_int32), ("phase1", C.c_int32), ("overlap", C.c_int32),
-                ("exchange", C.c_int32), ("exchange_timeout_ms", C.c_int32)]
+                ("exchange", C.c_int32), ("exchange_timeout_ms", C.c_int32),
+                ("host_share", C.c_double), ("host_threads", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -53,7 +54,8 @@ class Stats(C.Structure):
                 ("loop_ms_total", C.c_double), ("graph_launches", C.c_int64),
                 ("kernel_launches", C.c_int64), ("local_rows", C.c_int64), ("local_cols", C.c_int64),
                 ("local_ld", C.c_int64), ("col_offset", C.c_int64), ("bytes_per_pivot", C.c_int64),
-                ("path", C.c_int64)]
+                ("path", C.c_int64), ("host_cols", C.c_int64), ("host_ms_total", C.c_double),
+                ("host_wait_ms_total", C.c_double)]
 
 
 class SimplexError(RuntimeError):
@@ -198,7 +200,8 @@ class Simplex:
 
     def __init__(self, A, b, c, *, tol_opt=1e-7, tol_piv=1e-10, max_pivots=0, record_trace=True,
                  device=None, group=None, virtual_ranks=1, segment_pivots=0, time_kernels=False,
-                 lookahead=0, pivot_rule=DANTZIG, phase1=True, overlap=True, stream=None, exchange=0):
+                 lookahead=0, pivot_rule=DANTZIG, phase1=True, overlap=True, stream=None, exchange=0,
+                 host_share=0.0, host_threads=0):
         L = lib()
         if len(_shape(A)) != 2:
             raise ValueError("A must be a 2-D (m, n) array")
@@ -217,6 +220,8 @@ class Simplex:
         o.phase1 = 1 if phase1 else 0
         o.overlap = 1 if overlap else 0
         o.exchange = int(exchange)
+        o.host_share = float(host_share)
+        o.host_threads = int(host_threads)
         s = stream if stream is not None else _current_stream(o.device)
         o.stream = s if s else None
         self._idbuf = None

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsimplex.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "engine.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "engine.cpp", "host_lane.cpp")]
 DEPS = SOURCES + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
     [os.path.join(ROOT, "include", "libsimplex.h")]
 
@@ -64,10 +64,10 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     inc, lib = nccl_dirs()
     ncclso = sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0]
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xptxas", "-v",
-           "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared",
+           "-Xcompiler", "-fPIC,-O2,-ffp-contract=off,-fopenmp", "-shared",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
            *["-D" + d for d in defines], *SOURCES, "-o", target + ".tmp",
-           "-L", lib, "-l:" + os.path.basename(ncclso), "-Xlinker", "-rpath," + lib]
+           "-L", lib, "-l:" + os.path.basename(ncclso), "-Xlinker", "-rpath," + lib, "-lgomp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)

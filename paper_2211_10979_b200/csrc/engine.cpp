@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -24,6 +25,7 @@
 
 #include "../../include/libsimplex.h"
 #include "device.cuh"
+#include "host_lane.h"
 #include "kernels.h"
 
 namespace {
@@ -132,6 +134,16 @@ struct simplex_s {
   bool pdl = true;                  // programmatic dependent launch between pivot kernels
   bool force_nccl = false;          // exchange = 1 on one part: 1-rank NCCL exchange on one GPU
   bool small = false;               // the whole solve in one k_solve_small launch (tableau in smem)
+  // hybrid CPU lane (options.host_share > 0): the host owns the last columns
+  bool hybrid = false;
+  sx::HostLane lane;
+  double* h_slot = nullptr;         // pinned: the GPU part's candidate slot [v, k bits, col[0..m]]
+  double* h_wcol = nullptr;         // pinned: the winning column when the host lane wins
+  double* d_wcol = nullptr;         // ... its device copy (k_force stages it)
+  cudaEvent_t ev_slot = nullptr;
+  bool slot_ready = false;          // k_pack + D2H of the GPU candidate enqueued for the next pivot
+  std::vector<double> wcol;         // the winning column (host copy) of the current pivot
+  double host_ms = 0.0, host_wait_ms = 0.0;
   bool graphs_ready = false;
   cudaGraphExec_t seg[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> tev[2];
@@ -205,6 +217,9 @@ struct simplex_s {
   simplex_err enqueue_pivot(int slot, int t);
   simplex_err run(long long max_pivots, long long* done);
   simplex_err run_small(long long max_pivots, long long* done);
+  simplex_err run_hybrid(long long max_pivots, long long* done);
+  simplex_err load_lane(const double* A, const double* b, const double* c);
+  simplex_err enqueue_gpu_candidate();
   simplex_err flush_all();
   void release();
   simplex_err setup_p2p();
@@ -312,7 +327,24 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   if (arts > 0 && !opt.phase1) return fail(SIMPLEX_E_NEG_RHS, "b has a negative entry and phase1 = 0");
   // lookahead = 0 (automatic) on a tableau that fits in one CTA's shared memory, one column part,
   // no Phase I: the latency path — the whole solve in ONE k_solve_small launch
-  small = opt.lookahead == 0 && nparts == 1 && arts == 0 && !force_nccl &&
+  hybrid = opt.host_share > 0.0;
+  if (hybrid) {
+    if (!(opt.host_share < 1.0)) return fail(SIMPLEX_E_ARG, "host_share must be in [0, 1)");
+    if (nparts != 1) return fail(SIMPLEX_E_ARG, "host_share needs one GPU rank and no virtual ranks");
+    if (opt.lookahead > 1) return fail(SIMPLEX_E_ARG, "host_share needs lookahead 0 or 1 (one pivot per pass)");
+    if (arts > 0) return fail(SIMPLEX_E_ARG, "host_share needs b >= 0 (no Phase I)");
+    if (force_nccl) return fail(SIMPLEX_E_ARG, "host_share excludes exchange = 1");
+    lane.m = m;
+    lane.n = n;
+    lane.W = n + m + 1;
+    lane.hw = std::min<long long>(n + m - 1, std::max<long long>(1, std::llround(opt.host_share * (double)(n + m))));
+    lane.c0 = n + m - lane.hw;
+    lane.rule = opt.pivot_rule;
+    lane.threads = opt.host_threads;
+    look = 1;
+    overlap = false;
+  }
+  small = !hybrid && opt.lookahead == 0 && nparts == 1 && arts == 0 && !force_nccl &&
           sx::small_smem_bytes((int)(m + 1), (int)(n + m)) <= sx::small_smem_max();
   if (small) {
     look = 1;
@@ -341,6 +373,7 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
     sx::SlabView& v = sl.v;
     int64_t c0 = 0, w = 0;
     RET(simplex_partition(n + m + arts, nparts, p, &c0, &w));
+    if (hybrid) w = lane.c0;                     // the GPU keeps columns [0, c0 of the host lane)
     v.c0 = c0;
     v.w = (int)w;
     v.rows = (int)(m + 1);
@@ -435,6 +468,14 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
         CK(cudaMemset(v.probe, 0, sizeof(unsigned long long) * sx::kProbeSlots * 16 * sx::kProbeEv));
       }
     }
+  }
+  if (hybrid) {
+    RET(dalloc(&send, m + 3));
+    RET(dalloc(&d_wcol, m + 1));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h_slot), sizeof(double) * (size_t)(m + 3), cudaHostAllocDefault));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h_wcol), sizeof(double) * (size_t)(m + 1), cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&ev_slot, cudaEventDisableTiming));
+    wcol.resize((size_t)(m + 1));
   }
   RET(dalloc(&d_x, n));
   RET(dalloc(&d_y, m));
@@ -585,6 +626,7 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c, b
     CK(sx::launch_price0(v, opt.tol_opt, stream));
   }
   kernel_launches += (3 + (arts > 0 ? 1 : 0)) * nslabs;
+  if (hybrid) RET(load_lane(A, b, c));
   // validation result: every slab's error bits, one synchronisation (which also keeps the host
   // vectors above alive until their copies have run)
   for (int s = 0; s < nslabs; ++s)
@@ -602,6 +644,7 @@ simplex_err simplex_s::load(const double* A, const double* b, const double* c, b
     err = h_state[2].err;
   }
   status = SIMPLEX_RUNNING;
+  slot_ready = false;
   phase = arts > 0 ? 1 : 2;
   drive_pending = false;
   drive_done = 0;
@@ -780,6 +823,7 @@ simplex_err simplex_s::run(long long max_pivots, long long* done) {
   if (done) *done = 0;
   if (status != SIMPLEX_RUNNING) return SIMPLEX_OK;
   if (small) return run_small(max_pivots, done);
+  if (hybrid) return run_hybrid(max_pivots, done);
   RET(build_graphs());
   RET(enter());
   const long long stop_at = max_pivots > 0 ? it + max_pivots : LLONG_MAX;
@@ -890,6 +934,107 @@ simplex_err simplex_s::run_small(long long max_pivots, long long* done) {
   }
   status = h_state[2].status;
   it = h_state[2].it;
+  if (done) *done = it - it0;
+  return SIMPLEX_OK;
+}
+
+// ---- hybrid CPU lane (options.host_share, §IV)
+// The host lane's columns (host memory) from the caller's A / b / c (host or device pointers).
+simplex_err simplex_s::load_lane(const double* A, const double* b, const double* c) {
+  const long long ncols_a = std::max(0LL, std::min(n, lane.c0 + lane.hw) - lane.c0);
+  std::vector<double> Acols((size_t)(m * std::max(ncols_a, 1LL))), hb((size_t)m), hc((size_t)n);
+  if (ncols_a > 0)
+    CK(cudaMemcpy2DAsync(Acols.data(), sizeof(double) * ncols_a, A + lane.c0, sizeof(double) * n,
+                         sizeof(double) * ncols_a, m, cudaMemcpyDefault, stream));
+  CK(cudaMemcpyAsync(hb.data(), b, sizeof(double) * m, cudaMemcpyDefault, stream));
+  CK(cudaMemcpyAsync(hc.data(), c, sizeof(double) * n, cudaMemcpyDefault, stream));
+  CK(cudaStreamSynchronize(stream));
+  if (!lane.build(Acols.data(), ncols_a, hc.data(), hb.data()))
+    return fail(SIMPLEX_E_NONFINITE, "A, b or c contains NaN or Inf");
+  host_ms = host_wait_ms = 0.0;
+  return SIMPLEX_OK;
+}
+
+// The GPU part's Step-1 candidate and its column: write back any deferred pivot row, fold the
+// per-warp candidates (k_pack: [v, k, col[0..m]]), copy the slot to pinned host memory.
+simplex_err simplex_s::enqueue_gpu_candidate() {
+  const Slab& sl = slabs[0];
+  CK(sx::launch_pack(sl.v, send, 1, stream, false));
+  CK(cudaMemcpyAsync(h_slot, send, sizeof(double) * (size_t)(m + 3), cudaMemcpyDeviceToHost, stream));
+  CK(cudaEventRecord(ev_slot, stream));
+  ++kernel_launches;
+  slot_ready = true;
+  return SIMPLEX_OK;
+}
+
+// One pivot per iteration, the paper's per-iteration schedule: both lanes'
+// Step-1 candidates are folded on the host (the paper's "compared ... global maximum index"),
+// the ratio test runs on the host against the replicated rhs, and then the GPU applies the pivot
+// to its columns (k_flush, k_force with the winning column, k_update, and already the next
+// candidate: k_pack + D2H) WHILE the host cores apply it to theirs.  One host wait per pivot.
+simplex_err simplex_s::run_hybrid(long long max_pivots, long long* done) {
+  const long long it0 = it;
+  RET(enter());
+  const long long stop_at = max_pivots > 0 ? it + max_pivots : LLONG_MAX;
+  const Slab& sl = slabs[0];
+  CK(cudaEventRecord(ev_loop0, stream));
+  if (!slot_ready) RET(enqueue_gpu_candidate());
+  sx::HostCand hc = lane.candidate(opt.tol_opt);
+  auto now_ms = []() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  while (status == SIMPLEX_RUNNING && it < stop_at) {
+    const double t0 = now_ms();
+    CK(cudaEventSynchronize(ev_slot));
+    host_wait_ms += now_ms() - t0;
+    sx::HostCand g{h_slot[0], 0};
+    std::memcpy(&g.idx, &h_slot[1], sizeof(g.idx));
+    const bool gpu_wins = g.v < hc.v || (g.v == hc.v && g.idx < hc.idx);
+    const sx::HostCand win = gpu_wins ? g : hc;
+    if (win.idx == LLONG_MAX) {                                            // Step 1: optimal
+      status = SIMPLEX_OPTIMAL;
+      break;
+    }
+    const long long k = win.idx;
+    if (gpu_wins) std::memcpy(wcol.data(), h_slot + 2, sizeof(double) * (size_t)(m + 1));
+    else lane.column(k, wcol.data());
+    const sx::HostCand rb = lane.ratio(wcol.data(), opt.tol_piv);          // Step 2
+    if (rb.idx == LLONG_MAX) {
+      status = SIMPLEX_UNBOUNDED;
+      break;
+    }
+    if (it >= cap) {                                                       // reading c12
+      status = SIMPLEX_ITERATION_LIMIT;
+      break;
+    }
+    const long long r = rb.idx & 0xffffffffLL;
+    // Step 3 on the GPU's columns (asynchronous), then on the host lane's
+    const double* dcol = send + 2;
+    if (!gpu_wins) {
+      std::memcpy(h_wcol, wcol.data(), sizeof(double) * (size_t)(m + 1));
+      CK(cudaMemcpyAsync(d_wcol, h_wcol, sizeof(double) * (size_t)(m + 1), cudaMemcpyHostToDevice, stream));
+      dcol = d_wcol;
+    }
+    CK(sx::launch_flush(sl.v, stream));
+    CK(sx::launch_force(sl.v, (int)r, (int)k, dcol, stream));
+    CK(sx::launch_update(sl.v, sl.q, opt.tol_opt, sl.upd_grid, stream, false));
+    kernel_launches += 3;
+    RET(enqueue_gpu_candidate());
+    const double t1 = now_ms();
+    lane.pivot(r, k, wcol.data());
+    hc = lane.candidate(opt.tol_opt);
+    host_ms += now_ms() - t1;
+    ++it;
+  }
+  if (status != SIMPLEX_RUNNING) {
+    CK(sx::launch_set_status(sl.v.st, status, stream));
+    ++kernel_launches;
+  }
+  CK(cudaEventRecord(ev_loop1, stream));
+  CK(cudaEventSynchronize(ev_loop1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ev_loop0, ev_loop1));
+  loop_ms += ms;
   if (done) *done = it - it0;
   return SIMPLEX_OK;
 }
@@ -1007,6 +1152,9 @@ void simplex_s::release() {
   allocs.clear();
   if (h_state) cudaFreeHost(h_state);
   if (h_err) cudaFreeHost(h_err);
+  if (h_slot) cudaFreeHost(h_slot);
+  if (h_wcol) cudaFreeHost(h_wcol);
+  if (ev_slot) cudaEventDestroy(ev_slot);
   for (auto q : xs)
     if (q) cudaStreamDestroy(q);
   for (auto e : ev_join)
@@ -1120,6 +1268,14 @@ simplex_err simplex_get_solution(simplex_t* h, double* x, double* y, double* obj
     CK(sx::launch_extract(h->slabs[s].v, h->n, h->d_x, h->d_y, s == 0 ? h->d_obj : nullptr, h->stream));
   h->kernel_launches += h->nslabs;
   if (h->use_nccl()) NK(ncclAllReduce(h->d_y, h->d_y, (size_t)h->m, ncclFloat64, ncclSum, h->comm, h->stream));
+  std::vector<double> hy;
+  if (h->hybrid) {                          // the host lane's slack columns' entries of y
+    hy.assign((size_t)h->m, 0.0);
+    CK(cudaMemcpyAsync(hy.data(), h->d_y, sizeof(double) * h->m, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->lane.y_part(hy.data());
+    CK(cudaMemcpyAsync(h->d_y, hy.data(), sizeof(double) * h->m, cudaMemcpyHostToDevice, h->stream));
+  }
   if (x) CK(cudaMemcpyAsync(x, h->d_x, sizeof(double) * h->n, cudaMemcpyDefault, h->stream));
   if (y) CK(cudaMemcpyAsync(y, h->d_y, sizeof(double) * h->m, cudaMemcpyDefault, h->stream));
   double obj = 0.0;
@@ -1153,7 +1309,7 @@ simplex_err simplex_get_tableau(simplex_t* h, double* T_out, int64_t ld_out) {
   HANDLE_OK(h);
   if (!T_out) return fail(SIMPLEX_E_ARG, "NULL argument");
   DeviceGuard dg(h->device);
-  long long cols = 1;
+  long long cols = 1 + (h->hybrid ? h->lane.hw : 0);
   for (auto& sl : h->slabs) cols += sl.v.w;
   if (ld_out < cols) return fail(SIMPLEX_E_ARG, "ld_out smaller than the slab's logical columns");
   RET(h->enter());
@@ -1164,6 +1320,9 @@ simplex_err simplex_get_tableau(simplex_t* h, double* T_out, int64_t ld_out) {
     CK(cudaMemcpy2DAsync(T_out + (v.c0 - base), sizeof(double) * ld_out, v.T, sizeof(double) * v.ld,
                          sizeof(double) * v.w, v.rows, cudaMemcpyDefault, h->stream));
   }
+  if (h->hybrid)                                  // the host lane's columns
+    CK(cudaMemcpy2DAsync(T_out + h->lane.c0, sizeof(double) * ld_out, h->lane.T.data(), sizeof(double) * h->lane.hw,
+                         sizeof(double) * h->lane.hw, h->m + 1, cudaMemcpyDefault, h->stream));
   const sx::SlabView& v0 = h->slabs[0].v;
   CK(cudaMemcpy2DAsync(T_out + (cols - 1), sizeof(double) * ld_out, v0.T + v0.w, sizeof(double) * v0.ld,
                        sizeof(double), v0.rows, cudaMemcpyDefault, h->stream));
@@ -1187,6 +1346,7 @@ simplex_err simplex_tableau_hash(simplex_t* h, uint64_t* hash) {
   CK(cudaMemcpyAsync(&h->h_state[2].it, h->d_hash, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   std::memcpy(&v, &h->h_state[2].it, sizeof(v));
+  if (h->hybrid) v += h->lane.hash();             // the host lane's columns (same formula, mod 2^64)
   *hash = v;
   return SIMPLEX_OK;
 }
@@ -1201,14 +1361,17 @@ simplex_err simplex_get_stats(simplex_t* h, simplex_stats* s) {
   s->loop_ms_total = h->loop_ms;
   s->graph_launches = h->graph_launches;
   s->kernel_launches = h->kernel_launches;
-  long long cols = 1;
+  long long cols = 1 + (h->hybrid ? h->lane.hw : 0);
   for (auto& sl : h->slabs) cols += sl.v.w;
   s->local_rows = h->m + 1;
   s->local_cols = cols;
   s->local_ld = h->slabs[0].v.ld;
   s->col_offset = h->slabs[0].v.c0;
   s->bytes_per_pivot = 16LL * (h->m + 1) * cols;
-  s->path = h->small ? 1 : 0;
+  s->path = h->small ? 1 : h->hybrid ? 2 : 0;
+  s->host_cols = h->hybrid ? h->lane.hw : 0;
+  s->host_ms_total = h->host_ms;
+  s->host_wait_ms_total = h->host_wait_ms;
   return SIMPLEX_OK;
 }
 

@@ -682,14 +682,27 @@ constexpr int kLookCB = SX_LOOK_CB;                 // columns per load batch
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Distributed shared memory of another CTA may be written only once that CTA has started: every
+// cluster kernel arrives (relaxed) on entry and its FIRST cluster_min waits for all arrivals before
+// its DSMEM stores (compute-sanitizer racecheck: "write ... in a block that might not have entered
+// yet").  The arrive/wait split keeps the wait off the critical path in practice.
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
 // Cluster-wide lexicographic argmin, identical in every CTA of the cluster.  Each CTA
 // reduces its warps, then warp 0 writes the CTA's candidate straight into slot[rank] of
 // EVERY CTA's shared memory (DSMEM st.shared::cluster), one cluster barrier, and every
 // CTA folds its local copy.  `slot` is double-buffered by `ph` (a CTA can be at most one
 // reduction ahead of another), so two consecutive reductions never share a slot.
+// post_row (optional): thread 0 records a new pivot row — post_row[0] = post_val and its bit in
+// post_mark — after the CTA barrier that ends every thread's reads of the previous phase and before
+// the one that publishes the result (a write outside that window races with the phase's reads of
+// the same shared arrays: compute-sanitizer racecheck).
 __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const double* pf_rows = nullptr,
-                                            long long pf_ld = 0) {
+                                            long long pf_ld = 0, bool first = false, int* post_row = nullptr,
+                                            int post_val = 0, unsigned int* post_mark = nullptr) {
   __shared__ Cand sh_w[32];
   __shared__ Cand sh_res;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -698,7 +711,12 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const do
   asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(nct));
   c = warp_min(c);
   if (lane == 0) sh_w[wid] = c;
+  if (first) cluster_wait();                          // every CTA of the cluster has started
   __syncthreads();
+  if (post_row && threadIdx.x == 0) {
+    *post_row = post_val;
+    post_mark[post_val >> 5] |= 1u << (post_val & 31);
+  }
   if (wid == 0) {
     Cand t = lane < (int)(blockDim.x >> 5) ? sh_w[lane] : cand_none();
     t = warp_min(t);
@@ -748,6 +766,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
                                                            int bown, int bpre, int nqc, int nqr, double tol_opt,
                                                            double tol_piv) {
   pdl_launch_dependents();                            // the previous block's pass may start now
+  cluster_arrive_relaxed();                           // (waited for in the first cluster_min)
   DevState* st = s.st;
   __shared__ int sh_r[kMaxLook];                      // own pivot rows
   __shared__ int sh_rp[kMaxLook];                     // pivot rows of the previous block (bpre)
@@ -839,7 +858,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
       if (v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
     }
   }
-  best = cluster_min(best, slot, ph);                 // (its barriers also publish piv_mark)
+  best = cluster_min(best, slot, ph, nullptr, 0, true);   // (its barriers also publish piv_mark)
   ph ^= 1;
   SX_PROBE(1);
 
@@ -973,10 +992,6 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
         if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));  // Step 1 of t+1
       }
     }
-    if (threadIdx.x == 0) {                             // visible after cluster_min's barriers
-      sh_r[t] = r;
-      piv_mark[r >> 5] |= 1u << (r & 31);
-    }
     if (gtid == 0) {
       st->rsb[bown][t] = r;
       s.basis[r - 1] = (int)k;
@@ -990,7 +1005,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     c_prev = colTo + (size_t)t * rows;
     p_prev = prow;
     SX_PROBE(4 + 4 * t);
-    best = cluster_min(best, slot, ph);
+    best = cluster_min(best, slot, ph, nullptr, 0, false, &sh_r[t], r, piv_mark);   // (+ row r recorded)
     ph ^= 1;
     SX_PROBE(5 + 4 * t);
   }
@@ -1059,8 +1074,14 @@ __device__ __forceinline__ double ll_load(const unsigned long long* w, unsigned 
 __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __restrict__ T,
                                            const double* __restrict__ xin, double* __restrict__ xout, int nparts,
                                            long long xstride, int t, int S, int bown, int bpre, double tol_opt,
-                                           double tol_piv, const XPeers& xp) {
+                                           double tol_piv, const XPeers& xp, bool first_step) {
   DevState* st = s.st;
+  bool waited = !first_step;                          // the entry arrive still needs its wait
+#define MLOOK_RETURN             \
+  do {                           \
+    if (!waited) cluster_wait(); \
+    return;                      \
+  } while (0)
   __shared__ int sh_r[kMaxLook];                      // own pivot rows
   __shared__ int sh_rp[kMaxLook];                     // pivot rows of the previous bank
   __shared__ __align__(16) Cand slot[2 * 16];
@@ -1083,7 +1104,7 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
   long long it = st->it;
   if (t < 0 && gtid == 0) st->sb[bown] = 0;          // the block is empty until a pivot is taken
   const bool active = st->status == kRunning && it < st->stop_at;
-  if (!active) return;                                // uniform: every CTA reads the same state
+  if (!active) MLOOK_RETURN;                                // uniform: every CTA reads the same state
   const int spre = bpre >= 0 ? st->sb[bpre] : 0;
   // peer-memory exchange: the slots of this pivot carry sequence number xseq (every part has
   // published as many slots as this one); this launch publishes xseq + 1
@@ -1131,7 +1152,7 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
     }
     if (kb.idx == LLONG_MAX) {                                                  // optimal
       if (gtid == 0) st->status = kOptimal;
-      return;
+      MLOOK_RETURN;
     }
     const long long k = kb.idx;
     // Step 2 over all rows; the rhs gets the previous pivot first (at t = 0 of a pipelined
@@ -1154,18 +1175,19 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
         rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, basic));
       }
     }
-    rb = cluster_min(rb, slot, ph);
+    rb = cluster_min(rb, slot, ph, nullptr, 0, !waited);
+    waited = true;
     ph ^= 1;
     if (rb.idx == LLONG_MAX) {                                                  // unbounded
       if (gtid == 0) {
         st->status = kUnbounded;
         st->k = (int)k;
       }
-      return;
+      MLOOK_RETURN;
     }
     if (it >= st->cap) {                                                        // reading c12
       if (gtid == 0) st->status = kIterLimit;
-      return;
+      MLOOK_RETURN;
     }
     r = cand_row(rb.idx);
     const double p = xget(q, 2 + r);
@@ -1212,14 +1234,12 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
       }
       st->it = it + 1;
     }
-    if (threadIdx.x == 0) {
-      sh_r[t] = r;                                    // (visible after the next reduction)
-      piv_mark[r >> 5] |= 1u << (r & 31);
-    }
-    if (t + 1 >= S) return;                           // block complete: no candidate needed
+    if (t + 1 >= S) MLOOK_RETURN;                           // block complete: no candidate needed
   }
-  // this part's best column for the next pivot, and that column of the next tableau
-  best = cluster_min(best, slot, ph);
+  // this part's best column for the next pivot, and that column of the next tableau (pivot t's row
+  // r is recorded in sh_r / piv_mark inside the reduction, between its two CTA barriers)
+  best = cluster_min(best, slot, ph, nullptr, 0, !waited, t >= 0 ? &sh_r[t] : nullptr, r, piv_mark);
+  waited = true;
   // slot destinations: xout (NCCL send buffer or the one-GPU gather buffer), or buffer (t+1)&1
   // of every rank's gather buffer (peer memory)
   const long long off = 2 * ((long long)((t + 1) & 1) * xp.half + (long long)xp.part * xstride);   // LL words
@@ -1266,13 +1286,15 @@ __device__ __forceinline__ void mlook_step(const SlabView& s, const double* __re
   }
   if (xp.n > 0 && gtid == 0) st->xseq = xseq + 1;
 }
+#undef MLOOK_RETURN
 
 // One pivot t of a block per launch (t = -1: block start); the exchange between launches is
 // the NCCL allgather, plain stores (virtual slabs) or the peer-memory LL words.
 __global__ void __launch_bounds__(kLookThreads) k_mlook(SlabView s, const double* __restrict__ xin,
                                                        double* __restrict__ xout, int nparts, long long xstride,
                                                        int t, int S, double tol_opt, double tol_piv, XPeers xp) {
-  mlook_step(s, s.T, xin, xout, nparts, xstride, t, S, 0, -1, tol_opt, tol_piv, xp);
+  cluster_arrive_relaxed();                           // (waited for in the first cluster_min)
+  mlook_step(s, s.T, xin, xout, nparts, xstride, t, S, 0, -1, tol_opt, tol_piv, xp, true);
 }
 
 // The whole block's selection in ONE launch per part (peer-memory exchange only): the steps
@@ -1285,9 +1307,10 @@ __global__ void __launch_bounds__(kLookThreads) k_mblock(SlabView s, const doubl
                                                         double tol_piv, XPeers xp) {
   pdl_launch_dependents();            // (multi-part pipeline: the next part's selection and the slab
                                       //  passes are launched behind this one without waiting)
+  cluster_arrive_relaxed();                           // (waited for in the first cluster_min)
   for (int t = -1; t < S; ++t) {
     if (t >= 0) cluster_barrier();
-    mlook_step(s, T, nullptr, nullptr, nparts, xstride, t, S, bown, bpre, tol_opt, tol_piv, xp);
+    mlook_step(s, T, nullptr, nullptr, nparts, xstride, t, S, bown, bpre, tol_opt, tol_piv, xp, t < 0);
   }
 }
 

@@ -308,3 +308,62 @@ def test_wide_prefix_20000x40000(sx):
         assert np.array_equal(x, xs)
         assert h == int(g["tableau_hash"])
 
+
+
+def _wide_prefixes():
+    import glob
+    import re
+    out = {}
+    for p in glob.glob(os.path.join(GOLDEN_DIR, "dense_20000x40000_s1_p*.npz")):
+        mt = re.search(r"_p(\d+)\.npz$", p)
+        if mt:
+            out[int(mt.group(1))] = p
+    return out
+
+
+def test_wide_full_solve_20000x40000(sx):
+    """BASELINE config 5 (the north_star's largest tableau, 9.6 GB) solved to the end on the
+    library default path (the launch configuration bench.py times), checked against:
+      * EVERY oracle prefix golden written by scripts/make_golden_long.py (the row-parallel oracle,
+        bitwise equal to the single-thread one): the solve is stopped at exactly P pivots and its
+        trace, objective, y, x and whole-tableau digest compared bit for bit, then resumed;
+      * the oracle's full-solve golden when it exists (status, pivot count, whole trace, objective,
+        x, y, digest);
+      * always: a full optimality certificate from the RAW (A, b, c) in extended precision —
+        primal feasibility (Ax <= b + 1e-6, x >= -1e-9), dual feasibility (A^T y >= c - 1e-7,
+        y >= -1e-7) and strong duality |c^T x - b^T y| <= 1e-9 max(1, |obj|) (north_star)."""
+    A, b, c = lpgen.dense_lp(20000, 40000, 1)
+    pre = _wide_prefixes()
+    full = os.path.join(GOLDEN_DIR, "dense_20000x40000_s1.npz")
+    with sx.Simplex(A, b, c) as s:
+        done = 0
+        for P in sorted(pre):
+            d, st = s.iterate(P - done)
+            done += d
+            assert done == P and st == sx.RUNNING
+            g = np.load(pre[P])
+            k, r = s.trace()
+            x, y, obj, piv, _ = s.solution()
+            assert piv == P
+            assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"]), P
+            assert obj == float(g["objective"]) and np.array_equal(y, g["y"]), P
+            xs = np.zeros(40000)
+            xs[g["x_idx"]] = g["x_val"]
+            assert np.array_equal(x, xs), P
+            assert s.tableau_hash() == int(g["tableau_hash"]), P
+        st = s.solve()
+        x, y, obj, piv, _ = s.solution()
+        k, r = s.trace()
+        h = s.tableau_hash()
+    assert st == sx.OPTIMAL
+    if os.path.exists(full):
+        g = np.load(full)
+        assert piv == int(g["pivots"]) and st == int(g["status"])
+        assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
+        assert obj == float(g["objective"]) and np.array_equal(y, g["y"])
+        xs = np.zeros(40000)
+        xs[g["x_idx"]] = g["x_val"]
+        assert np.array_equal(x, xs) and h == int(g["tableau_hash"])
+    cert = oracle.certificate(A, b, c, x, y)
+    assert not cert.violations, cert.violations
+    assert cert.gap_rel <= 1e-9
