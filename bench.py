@@ -156,6 +156,11 @@ def ncu_duration(workload, nranks, look=1):
     return e.get("ncu_duration_us") if e else None
 
 
+def ncu_l2(workload, nranks, look=1):
+    e = ncu_entry(workload, nranks, look)
+    return e.get("l2_bytes_per_launch") if e else None
+
+
 def ncu_traffic(workload, nranks, look=1):
     """dram read+write bytes per pass launch (k_update, or k_update_s for look > 1) from a
     committed ncu --set full capture."""
@@ -682,6 +687,8 @@ def main():
                                     "selection of the next block)") if look > 1 else
                                    "k_update (fused row-scale + rank-1 update)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "frac_of_8tbs_spec": achieved / 8000.0,
+                         "l2_bytes_per_launch": ncu_l2(args.workload, world, look),
                          "per_rank_frac": per_rank_frac,
                          "peak_source": peak_src, "traffic": ncu_traffic(args.workload, world, look),
                          "bytes_per_launch": st.bytes_per_pivot,

@@ -704,7 +704,6 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const do
                                             long long pf_ld = 0, bool first = false, int* post_row = nullptr,
                                             int post_val = 0, unsigned int* post_mark = nullptr) {
   __shared__ Cand sh_w[32];
-  __shared__ Cand sh_res;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned int rank, nct;
   asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -736,13 +735,11 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const do
                    : "memory");
   }
   cluster_barrier();
-  if (wid == 0) {
-    Cand t = lane < (int)nct ? slot[ph * 16 + lane] : cand_none();
-    t = warp_min(t);
-    if (lane == 0) sh_res = t;
-  }
-  __syncthreads();
-  return sh_res;
+  // every warp folds the nct slots itself (a CTA barrier to broadcast warp 0's fold would cost
+  // more than the redundant 32-lane argmin); the cluster barrier above already ordered every
+  // shared-memory write of the phase for all threads
+  Cand t = lane < (int)nct ? slot[ph * 16 + lane] : cand_none();
+  return warp_min(t);
 }
 
 
