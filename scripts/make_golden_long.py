@@ -31,7 +31,8 @@ sys.path.insert(0, ROOT)
 import lpgen  # noqa: E402
 import oracle  # noqa: E402
 
-GOLDEN = os.path.join(ROOT, "tests", "golden")
+GOLDEN = os.environ.get("GOLDEN_OUT") or os.path.join(ROOT, "tests", "golden")   # GOLDEN_OUT: e.g. gpurun_out/golden
+os.makedirs(GOLDEN, exist_ok=True)
 
 
 def save_golden(tag, m, n, seed, prefix, status, pivots, T, basis, tk, tr, secs, threads):
@@ -68,7 +69,7 @@ def main():
     ap.add_argument("--ckpt", default=None)
     ap.add_argument("--chunk", type=int, default=512)
     ap.add_argument("--milestones", default="4096,16384,65536")
-    ap.add_argument("--ckpt-every", type=int, default=8192)
+    ap.add_argument("--ckpt-every", type=int, default=8192, help="0: never checkpoint")
     a = ap.parse_args()
     m, n, seed = a.m, a.n, a.seed
     threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
@@ -102,14 +103,14 @@ def main():
         with open(os.path.join(GOLDEN, tag + "_progress.json"), "w") as f:
             json.dump(dict(pivots_done=it, status=oracle.STATUS_NAME[status], oracle_seconds=secs,
                            s_per_pivot=secs / max(it, 1), threads=threads), f)
-        ref = os.path.join(GOLDEN, f"{tag}_p{it}.npz")
-        if status == oracle.RUNNING and it not in milestones and os.path.exists(ref):
-            # an existing prefix golden from the single-thread build: must agree bit for bit
+        ref = os.path.join(ROOT, "tests", "golden", f"{tag}_p{it}.npz")
+        if status == oracle.RUNNING and os.path.exists(ref):
+            # an existing committed prefix golden (an earlier oracle run): must agree bit for bit
             g = np.load(ref)
             same = (np.array_equal(np.array(tk, np.int32), g["trace_k"])
                     and np.array_equal(np.array(tr, np.int32), g["trace_r"])
                     and oracle.tableau_hash(T) == int(g["tableau_hash"]))
-            print(f"check vs single-thread prefix golden p{it}: {'identical' if same else 'DIFFERENT'}",
+            print(f"check vs committed prefix golden p{it}: {'identical' if same else 'DIFFERENT'}",
                   flush=True)
             if not same:
                 sys.exit(1)
@@ -117,7 +118,7 @@ def main():
             if it == ms and status == oracle.RUNNING:
                 save_golden(f"{tag}_p{ms}", m, n, seed, ms, status, it, T, basis,
                             np.array(tk, np.int32), np.array(tr, np.int32), secs, threads)
-        if status == oracle.RUNNING and it - last_ck >= a.ckpt_every:
+        if status == oracle.RUNNING and a.ckpt_every > 0 and it - last_ck >= a.ckpt_every:
             T.tofile(os.path.join(ck, "T.f64.tmp"))
             os.replace(os.path.join(ck, "T.f64.tmp"), os.path.join(ck, "T.f64"))
             np.save(os.path.join(ck, "basis.npy"), basis)
