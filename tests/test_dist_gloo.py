@@ -7,7 +7,8 @@ tests/test_gpu_parity.py (virtual ranks and a real 1-rank NCCL communicator).  H
   * the per-rank Step-1 candidates folded lexicographically equal the sequential
     Step 1 over the whole row, i.e. the protocol
     the device implements is exact, with the oracle's Step 1 on each rank's slab;
-  * bench.py's max-over-ranks timing reduction.
+  * bench.py's max-over-ranks timing reduction, its sum and gather helpers, and the rank-0-only
+    oracle cpu_baseline leg with the other ranks waiting at a barrier.
 """
 import os
 import socket
@@ -69,6 +70,14 @@ def _worker(rank, world, port, q):
         # (4) bench timing reduction: max over ranks
         import bench
         out["tmax"] = bench.reduce_max(10.0 * (rank + 1), world, torch.device("cpu"))
+        out["tsum"] = bench.reduce_sum(1.5 * (rank + 1), world, torch.device("cpu"))
+        # (5) the per-rank roofline fractions gathered to every rank (bench.gather_list)
+        out["fracs"] = bench.gather_list(0.9 + 0.01 * rank, world)
+        # (6) the cpu_baseline leg runs on rank 0 only while the others wait at a barrier
+        if rank == 0:
+            A0, b0, c0_ = lpgen.dense_lp(64, 64, 1)
+            out["cpu"] = bench.cpu_baseline(A0, b0, c0_, 0.3)["kind"]
+        dist.barrier()
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -91,6 +100,9 @@ def test_gloo_world2(world):
         assert out["ids_equal"]
         assert out["fold_ok"]
         assert out["tmax"] == 10.0 * world
+        assert out["tsum"] == 1.5 * world * (world + 1) / 2
+        assert out["fracs"] == [0.9 + 0.01 * q for q in range(world)]
+        assert (out.get("cpu") == "oracle") == (r == 0)
         parts = out["parts"]
         assert parts == res[0]["parts"]
         assert parts[0][0] == 0 and sum(w for _, w in parts) == 37 + 53
