@@ -95,6 +95,9 @@ def parse():
                     help="entering/leaving rule (bland = SURVEY.md §8(f) NEXT #3)")
     ap.add_argument("--single-pass-pivots", type=int, default=1000,
                     help="pivots of the one-pivot-per-pass k_update roofline window (0: skip)")
+    ap.add_argument("--exchange", type=int, default=0,
+                    help="simplex_options.exchange for N > 1 (0: peer memory when reachable, else NCCL; "
+                         "1: NCCL); a peer-memory failure at N > 1 falls back to 1 and says so")
     ap.add_argument("--largest", default="20000x40000",
                     help="the north_star's largest tableau: a sub-record of simplex_iterate windows "
                          "('none' to skip; skipped when it is the main workload)")
@@ -377,7 +380,7 @@ def gather_list(v, world):
     return out
 
 
-def largest_leg(args, world, group, dev, peak, barrier):
+def largest_leg(args, world, group, dev, peak, barrier, exchange=0):
     """The north_star's largest tableau (20000x40000 by default) as a sub-record of every line:
     pivots/s as the median of 3 simplex_iterate windows ("median of 3 windows
     ... driven by simplex_iterate"), the device-timed pass roofline, and the first pivots checked
@@ -390,7 +393,7 @@ def largest_leg(args, world, group, dev, peak, barrier):
     A, b, c = lpgen.dense_lp(m, n, args.seed)
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    s = sx.Simplex(A, b, c, group=group, time_kernels=True)
+    s = sx.Simplex(A, b, c, group=group, time_kernels=True, exchange=exchange)
     del A
     barrier()
     t_create = time.perf_counter() - t0
@@ -472,8 +475,20 @@ def main():
     torch.cuda.synchronize()
 
     rule = sx.BLAND if args.pivot_rule == "bland" else sx.DANTZIG
-    solver = sx.Simplex(dA, db, dc, group=group, lookahead=args.lookahead, pivot_rule=rule,
-                        overlap=not args.no_overlap)
+    exchange = args.exchange
+    fallback = None
+
+    def make(**kw):
+        return sx.Simplex(dA, db, dc, group=group, pivot_rule=rule, exchange=exchange, **kw)
+
+    try:
+        solver = make(lookahead=args.lookahead, overlap=not args.no_overlap)
+    except sx.SimplexError as e:
+        if world <= 1 or exchange == 1:
+            raise
+        fallback = f"exchange {exchange} failed at create ({e}); NCCL exchange (1) used"
+        exchange = 1
+        solver = make(lookahead=args.lookahead, overlap=not args.no_overlap)
     st = solver.stats()
     small = st.path == 1                                     # one-CTA shared-memory solve (k_solve_small)
     tableau_bytes = 8 * (m + 1) * (n + m + 1)
@@ -503,13 +518,31 @@ def main():
     pre = golden_prefixes(m, n, args.seed) if not suffix else {}
     if not os.path.exists(gpath) and pre:
         P = max(pre)
-        solver.iterate(P)
+        try:
+            solver.iterate(P)
+        except sx.SimplexError as e:             # e.g. a peer-memory exchange timeout on N > 1
+            if world <= 1 or exchange == 1:
+                raise
+            fallback = f"exchange {exchange} failed in the first solve ({e}); NCCL exchange (1) used"
+            exchange = 1
+            solver.close()
+            solver = make(lookahead=args.lookahead, overlap=not args.no_overlap)
+            solver.iterate(P)
         ok = check_prefix(solver, np.load(pre[P]), P)
         parity = {"checked": True, "vs": os.path.relpath(pre[P], ROOT), "prefix_pivots": P,
                   "bitwise_trace_objective_y_tableau_digest": ok}
         if not ok:
             raise SystemExit(f"PARITY FAILURE vs {pre[P]}")
-    status, obj, piv = one_step(reload=False)
+    try:
+        status, obj, piv = one_step(reload=False)
+    except sx.SimplexError as e:
+        if world <= 1 or exchange == 1:
+            raise
+        fallback = f"exchange {exchange} failed in the first solve ({e}); NCCL exchange (1) used"
+        exchange = 1
+        solver.close()
+        solver = make(lookahead=args.lookahead, overlap=not args.no_overlap)
+        status, obj, piv = one_step(reload=False)
     k, r = solver.trace()
     if os.path.exists(gpath):
         g = np.load(gpath)
@@ -556,8 +589,7 @@ def main():
     # on the device (%globaltimer in the kernel: first CTA start -> last CTA end, the production
     # launch sequence); the one-pivot k_update with CUDA events around every launch (event nodes in
     # the captured graph, on the stream the kernel runs on).  Kept out of the value steps.
-    prof = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule,
-                      overlap=not args.no_overlap)
+    prof = make(time_kernels=True, lookahead=args.lookahead, overlap=not args.no_overlap)
     barrier()
     window = min(piv, args.roofline_pivots)
     prof.iterate(window)
@@ -597,7 +629,7 @@ def main():
     # ---- the one-pivot-per-pass kernel (k_update) measured the same way, for reference
     single = None
     if (look > 1 or small) and args.single_pass_pivots > 0:
-        p1 = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=1, pivot_rule=rule)
+        p1 = make(time_kernels=True, lookahead=1)
         barrier()
         p1.iterate(min(piv, args.single_pass_pivots))
         barrier()
@@ -612,8 +644,7 @@ def main():
     # ---- the rank-s pass alone (select-then-pass schedule: all SMs, in place), for reference
     alone = None
     if look > 1 and not args.no_overlap and args.single_pass_pivots > 0 and world == 1:
-        p2 = sx.Simplex(dA, db, dc, group=group, time_kernels=True, lookahead=args.lookahead, pivot_rule=rule,
-                        overlap=False)
+        p2 = make(time_kernels=True, lookahead=args.lookahead, overlap=False)
         barrier()
         p2.iterate(min(piv, args.roofline_pivots))
         barrier()
@@ -661,7 +692,7 @@ def main():
     # ---- the largest tableau (north_star scaling target) as a sub-record
     largest = None
     if args.largest not in ("none", "", args.workload):
-        largest = largest_leg(args, world, group, dev, peak, barrier)
+        largest = largest_leg(args, world, group, dev, peak, barrier, exchange)
 
     # ---- the oracle on the host, rank 0, at every N (the other ranks wait at the barrier)
     cpu = None
@@ -683,7 +714,11 @@ def main():
                                     "(two tableau buffers)" if look > 1 and not args.no_overlap else
                                     "select, then pass" if look > 1 else "one pivot per pass"),
                        "time_to_solve_ms": total_ms / args.steps, "time_to_solve_us": 1e3 * total_ms / args.steps,
-                       "parallelism": f"column slabs x{world}" + (" (candidate columns exchanged over peer memory per pivot)" if world > 1 else ""),
+                       "parallelism": f"column slabs x{world}" + ((" (candidate columns exchanged over peer memory per pivot)"
+                                                                   if exchange != 1 else
+                                                                   " (candidate columns exchanged by NCCL allgather per pivot)")
+                                                                  if world > 1 else ""),
+                       "exchange": exchange if world > 1 else None, "exchange_fallback": fallback,
                        "l2": ("tableau %.2f GB > L2 %d MB: inputs larger than L2" % (tableau_bytes / 1e9, l2 >> 20))
                        if flush is None else "L2 flushed (write 2xL2) before every timed step",
                        "step": "reset (build Table I from device-resident A,b,c) + solve + extract"},

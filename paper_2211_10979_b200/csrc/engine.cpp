@@ -566,14 +566,34 @@ simplex_err simplex_s::setup_p2p() {
     NK(ncclAllGather(d_h + hb * rank, d_h, hb, ncclUint8, comm, stream));
     CK(cudaMemcpyAsync(hh.data(), d_h, hb * nranks, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
-    for (int r = 0; r < nranks; ++r) {
+    int opened = 1;                                  // every rank must agree that every mapping worked
+    for (int r = 0; r < nranks && opened; ++r) {
       if (r == rank) continue;
       cudaIpcMemHandle_t a;
       std::memcpy(&a, hh.data() + hb * r, sizeof(a));
       void* pa = nullptr;
-      CK(cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess));
+      if (cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        opened = 0;
+        break;
+      }
       ipc_open.push_back(pa);
       px[(size_t)r] = static_cast<unsigned long long*>(pa);
+    }
+    {
+      int* d_op = reinterpret_cast<int*>(d_h);
+      CK(cudaMemcpyAsync(d_op, &opened, sizeof(int), cudaMemcpyHostToDevice, stream));
+      NK(ncclAllReduce(d_op, d_op, 1, ncclInt32, ncclMin, comm, stream));
+      CK(cudaMemcpyAsync(&opened, d_op, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+    }
+    if (!opened) {                                   // a CUDA-IPC mapping failed somewhere: NCCL instead
+      for (void* pa : ipc_open) cudaIpcCloseMemHandle(pa);
+      ipc_open.clear();
+      if (opt.exchange >= 2) return fail(SIMPLEX_E_CUDA, "exchange = 2/3 (peer memory) but a CUDA-IPC mapping failed");
+      p2p = false;
+      RET(dalloc(&send, xstride));
+      return SIMPLEX_OK;
     }
     // no rank may store into a peer before that peer's buffer is zeroed: the memset above is
     // ordered before this allreduce on every rank
