@@ -56,7 +56,7 @@ typedef enum {
     SIMPLEX_OK = 0,
     SIMPLEX_E_ARG = -1,        /* NULL pointer, m < 1, n < 1, bad option, shape mismatch   */
     SIMPLEX_E_NONFINITE = -2,  /* NaN or Inf in A, b or c                                   */
-    SIMPLEX_E_NEG_RHS = -3,    /* some b_i < 0 with phase1 = 0, or on more than one part     */
+    SIMPLEX_E_NEG_RHS = -3,    /* some b_i < 0 with phase1 = 0 (phase1 = 1, the default, solves it) */
     SIMPLEX_E_OOM = -4,        /* device or pinned host allocation failed                   */
     SIMPLEX_E_CUDA = -5,       /* CUDA runtime error, or no CUDA device                     */
     SIMPLEX_E_NCCL = -6,       /* NCCL error (multi-GPU)                                    */
@@ -171,7 +171,8 @@ typedef struct {
 void simplex_default_options(simplex_options* o);
 
 /* Allocate a handle on the GPU, copy (A, b, c), build Table I.
- *   A: m x n row-major (lda = n), b: m (all >= 0), c: n — host or device memory.
+ *   A: m x n row-major (lda = n), b: m (entries < 0 run Phase I, options.phase1), c: n — host or
+ *   device memory.
  *   opt may be NULL (defaults, 1 GPU).  Errors: ARG, NONFINITE, NEG_RHS, OOM, CUDA,
  *   NCCL.  On error *out is NULL. */
 simplex_err simplex_create(simplex_t** out, int64_t m, int64_t n,

@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(kThreads) k_select(SlabView s, XView x, double
 }
 
 // ------------------------------------------------------------------ a4 (+a1): update
-// Column-owner, row-strided schedule (measured best on B200, profiles/ubench_update_r01.txt):
+// Column-owner, row-strided schedule (measured best on B200 with scripts/ubench_update.cu):
 // thread t owns the double2 column pair jp = t mod (ld/2) and rows k0 = t div (ld/2),
 // k0+q, k0+2q, ... where q = (resident threads) div (ld/2).  At any moment all resident
 // threads sweep q consecutive rows, so the chip-wide access front is one contiguous
