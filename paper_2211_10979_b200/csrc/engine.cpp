@@ -392,12 +392,15 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
         // slab passes (overlap = 1) when two tableau buffers per slab fit
         mblock = opt.exchange != 3 && sx::mblock_max_clusters(sl.look_grid, v.rows) >= nslabs;
         if (mblock && opt.overlap != 0) {
-          // pipelined only up to 2.5 GB of slab stream per block: beyond it the one-GPU emulation
-          // measured the selection starved by the concurrent passes
+          // pipelined whenever two buffers per slab fit; with SEVERAL slabs on this GPU (virtual
+          // ranks) only up to 2.5 GB of slab stream per block: beyond it the one-GPU emulation, where
+          // the P passes share one HBM, measured the selections starved by the concurrent passes
+          // (DESIGN.md §8).  One slab per GPU (real ranks) is the single-part case of §9e, where the
+          // pipeline is measured to help at every size (20000x40000: 3.44 vs 3.75 ms per block).
           size_t free_b = 0, total_b = 0;
           CK(cudaMemGetInfo(&free_b, &total_b));
           mpipe = 2.2 * 8.0 * (double)v.rows * (double)v.ld * nslabs <= (double)free_b &&
-                  16.0 * (double)v.rows * (double)v.ld <= 2.5e9;
+                  (nslabs == 1 || 16.0 * (double)v.rows * (double)v.ld <= 2.5e9);
         }
       }
       // k_update_s: column chunks of cw doubles x row groups; all CTAs resident
