@@ -70,6 +70,9 @@ def main():
     ap.add_argument("--chunk", type=int, default=512)
     ap.add_argument("--milestones", default="4096,16384,65536")
     ap.add_argument("--ckpt-every", type=int, default=8192, help="0: never checkpoint")
+    ap.add_argument("--max-seconds", type=float, default=0.0,
+                    help="> 0: checkpoint and exit (code 3) once this much wall time has passed, so a run "
+                         "can be split over several time-limited sessions that share the checkpoint dir")
     a = ap.parse_args()
     m, n, seed = a.m, a.n, a.seed
     threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
@@ -93,7 +96,23 @@ def main():
         tk, tr, it, secs = [], [], 0, 0.0
     last_ck = it
     status = oracle.RUNNING
+    wall0 = time.time()
+
+    def checkpoint():
+        T.tofile(os.path.join(ck, "T.f64.tmp"))
+        os.replace(os.path.join(ck, "T.f64.tmp"), os.path.join(ck, "T.f64"))
+        np.save(os.path.join(ck, "basis.npy"), basis)
+        np.save(os.path.join(ck, "trace_k.npy"), np.array(tk, np.int32))
+        np.save(os.path.join(ck, "trace_r.npy"), np.array(tr, np.int32))
+        json.dump(dict(it=it, secs=secs), open(state + ".tmp", "w"))
+        os.replace(state + ".tmp", state)
+        print(f"checkpoint at pivot {it}, {secs:.0f} s", flush=True)
+
     while status == oracle.RUNNING:
+        if a.max_seconds > 0 and time.time() - wall0 > a.max_seconds:
+            checkpoint()
+            print(f"paused at pivot {it} after {time.time() - wall0:.0f} s of this session", flush=True)
+            sys.exit(3)
         t0 = time.perf_counter()
         stop = min([it + a.chunk] + [ms for ms in milestones if ms > it])
         status, it, k, r = oracle.iterate(T, basis, it, stop_at=stop, parallel=True)
@@ -119,14 +138,8 @@ def main():
                 save_golden(f"{tag}_p{ms}", m, n, seed, ms, status, it, T, basis,
                             np.array(tk, np.int32), np.array(tr, np.int32), secs, threads)
         if status == oracle.RUNNING and a.ckpt_every > 0 and it - last_ck >= a.ckpt_every:
-            T.tofile(os.path.join(ck, "T.f64.tmp"))
-            os.replace(os.path.join(ck, "T.f64.tmp"), os.path.join(ck, "T.f64"))
-            np.save(os.path.join(ck, "basis.npy"), basis)
-            np.save(os.path.join(ck, "trace_k.npy"), np.array(tk, np.int32))
-            np.save(os.path.join(ck, "trace_r.npy"), np.array(tr, np.int32))
-            json.dump(dict(it=it, secs=secs), open(state, "w"))
+            checkpoint()
             last_ck = it
-            print(f"checkpoint at pivot {it}, {secs:.0f} s", flush=True)
     save_golden(tag, m, n, seed, -1, status, it, T, basis, np.array(tk, np.int32),
                 np.array(tr, np.int32), secs, threads)
 
