@@ -161,7 +161,9 @@ typedef struct {
     int64_t bytes_per_pivot;     /* algorithmic bytes of one update: 16*(m+1)*local_cols     */
     int64_t path;                /* 0: device loop of captured CUDA-graph segments; 1: the whole
                                     solve in one single-CTA launch with the tableau in shared
-                                    memory (small tableaux, lookahead = 0); 2: hybrid CPU lane  */
+                                    memory (small tableaux, lookahead = 0); 2: hybrid CPU lane;
+                                    3: as 0 with the shared-memory look-ahead selection k_look2
+                                    (one column part, m + 1 <= 4096 and pitch <= 8192 doubles) */
     int64_t host_cols;           /* columns of the hybrid CPU lane (0: none)                  */
     double  host_ms_total;       /* host time spent updating the CPU lane's columns           */
     double  host_wait_ms_total;  /* host time spent waiting for the GPU's candidate per pivot */

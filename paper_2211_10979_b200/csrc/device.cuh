@@ -11,6 +11,7 @@
 //   rcand    ratio-test block candidates
 #pragma once
 #include <cstdint>
+#include <vector_types.h>
 
 namespace sx {
 
@@ -115,6 +116,14 @@ struct SlabView {
   double* R0;          // [ld]              current objective row during selection
   double* RHS;         // [rows]            current rhs column during selection
   Cand* pcand;         // [look-ahead CTAs] Step-1 candidates per CTA
+  // k_look2: hand-off of each launch's own-bank chain operands to the next launch
+  // (2 banks x [own column slots q][8 pairs][G threads] + [own row slots][8][G], double2); NULL and
+  // look_nt = 0: the selection is k_lookahead
+  double2* hand;
+  int look_nt;         // threads per CTA of k_look2 (0: k_lookahead)
+  int look_qc, look_qr;     // k_look2 instantiation: own column / row slots per thread
+  int look_os;              // 1: its own-bank operands in shared memory, 0: in the hand-off slots
+  int look_nqc, look_nqr;   // own columns / rows per thread actually used (hand-off layout)
   unsigned long long* probe;   // experiment hook (SIMPLEX_PROBE): selection phase timestamps, else NULL
   int time_pass;       // 1: k_update_s times itself on the device (DevState pass_*) — the way to
                        // time the pipelined pass WHILE the selection runs next to it (event nodes
@@ -123,9 +132,10 @@ struct SlabView {
 
 // k_lookahead phase timestamps (experiment hook): per launch slot (64), per CTA (16),
 // kProbeEv %globaltimer stamps: start, after the first reduction, then per pivot t
-// [phase A done, reduction A done, phase B done, reduction B done].
+// [phase A loads arrived, phase A done, CTA reduction A done, cluster barrier A done, reduction A
+// done, phase B loads arrived, phase B done, CTA reduction B, cluster barrier B, reduction B done].
 constexpr int kProbeSlots = 64;
-constexpr int kProbeEv = 2 + 4 * kMaxLook;
+constexpr int kProbeEv = 2 + 10 * kMaxLook;
 
 // Where k_select takes the entering column from.
 struct XView {

@@ -465,6 +465,13 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
       RET(dalloc(&v.R0, v.ld));
       RET(dalloc(&v.RHS, v.rows));
       RET(dalloc(&v.pcand, sl.look_grid));
+      if (nparts == 1 && !hybrid && !force_nccl) {
+        // k_look2 when the own-bank chain operands fit in shared memory; the
+        // experiment build can force k_lookahead (SIMPLEX_LOOK_V1=1)
+        const char* e1 = sx::experiment_env("SIMPLEX_LOOK_V1");
+        const long long hn = (e1 && e1[0] == '1') ? 0 : sx::look2_prepare(&v, sl.look_grid);
+        if (hn > 0) RET(dalloc(&v.hand, (size_t)hn));
+      }
       v.time_pass = time_pass() ? 1 : 0;
       if (sx::experiment_env("SIMPLEX_PROBE")) {          // experiment hook: selection phase stamps
         RET(dalloc(&v.probe, (size_t)sx::kProbeSlots * 16 * sx::kProbeEv));
@@ -1391,7 +1398,7 @@ simplex_err simplex_get_stats(simplex_t* h, simplex_stats* s) {
   s->local_ld = h->slabs[0].v.ld;
   s->col_offset = h->slabs[0].v.c0;
   s->bytes_per_pivot = 16LL * (h->m + 1) * cols;
-  s->path = h->small ? 1 : h->hybrid ? 2 : 0;
+  s->path = h->small ? 1 : h->hybrid ? 2 : (!h->slabs.empty() && h->slabs[0].v.look_nt > 0) ? 3 : 0;
   s->host_cols = h->hybrid ? h->lane.hw : 0;
   s->host_ms_total = h->host_ms;
   s->host_wait_ms_total = h->host_wait_ms;

@@ -702,7 +702,8 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 // the same shared arrays: compute-sanitizer racecheck).
 __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const double* pf_rows = nullptr,
                                             long long pf_ld = 0, bool first = false, int* post_row = nullptr,
-                                            int post_val = 0, unsigned int* post_mark = nullptr) {
+                                            int post_val = 0, unsigned int* post_mark = nullptr,
+                                            unsigned long long* pr = nullptr) {
   __shared__ Cand sh_w[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned int rank, nct;
@@ -719,6 +720,11 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const do
   if (wid == 0) {
     Cand t = lane < (int)(blockDim.x >> 5) ? sh_w[lane] : cand_none();
     t = warp_min(t);
+    if (pr && lane == 0) {                              // experiment probe: CTA reduction done
+      unsigned long long tnow;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow) : "l"(t.idx));
+      pr[0] = tnow;
+    }
     if (lane < (int)nct) {
       const uint32_t local = smem_u32(slot + ph * 16 + rank);
       uint32_t remote;
@@ -735,6 +741,11 @@ __device__ __forceinline__ Cand cluster_min(Cand c, Cand* slot, int ph, const do
                    : "memory");
   }
   cluster_barrier();
+  if (pr && threadIdx.x == 0) {                         // experiment probe: cluster barrier done
+    unsigned long long tnow;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+    pr[1] = tnow;
+  }
   // every warp folds the nct slots itself (a CTA barrier to broadcast warp 0's fold would cost
   // more than the redundant 32-lane argmin); the cluster barrier above already ordered every
   // shared-memory write of the phase for all threads
@@ -797,6 +808,14 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     if (prb && threadIdx.x == 0) {                                                  \
       unsigned long long tnow;                                                      \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));                      \
+      prb[e] = tnow;                                                                \
+    }                                                                               \
+  } while (0)
+#define SX_PROBE_DEP(e, dep)                                                        \
+  do {                                                                              \
+    if (prb && threadIdx.x == 0) {                                                  \
+      unsigned long long tnow;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow) : "d"(dep));           \
       prb[e] = tnow;                                                                \
     }                                                                               \
   } while (0)
@@ -890,6 +909,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
 #pragma unroll
         for (int u = 0; u < kMaxLook; ++u) cub[b][u] = v && u < t ? colTo[(size_t)u * rows + i] : 0.0;
       }
+      if (i0 == gtid) SX_PROBE_DEP(2 + 10 * t, xb[0] + hb[0] + cpb[0] + cub[0][0] + cub[0][kMaxLook - 1]);
 #pragma unroll
       for (int b = 0; b < kLookRB; ++b) {
         const long long i = i0 + b * gthreads;
@@ -925,10 +945,10 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
           rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h, x), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
       }
     }
-    SX_PROBE(2 + 4 * t);
-    rb = cluster_min(rb, slot, ph, T, ld);
+    SX_PROBE(3 + 10 * t);
+    rb = cluster_min(rb, slot, ph, T, ld, false, nullptr, 0, nullptr, prb ? prb + 4 + 10 * t : nullptr);
     ph ^= 1;
-    SX_PROBE(3 + 4 * t);
+    SX_PROBE(6 + 10 * t);
     if (rb.idx == LLONG_MAX) {                                                 // unbounded
       status = kUnbounded;
       if (gtid == 0) st->k = (int)k;
@@ -965,6 +985,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
 #pragma unroll
         for (int u = 0; u < kMaxLook; ++u) pub[b][u] = v && u < t ? prowO[(long long)u * ld + j] : 0.0;
       }
+      if (j0 == gtid) SX_PROBE_DEP(7 + 10 * t, xb[0] + r0b[0] + pub[0][0] + pub[0][kMaxLook - 1]);
 #pragma unroll
       for (int b = 0; b < kLookCB; ++b) {
         const long long j = j0 + b * gthreads;
@@ -1001,12 +1022,440 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     r_prev = r;
     c_prev = colTo + (size_t)t * rows;
     p_prev = prow;
-    SX_PROBE(4 + 4 * t);
-    best = cluster_min(best, slot, ph, nullptr, 0, false, &sh_r[t], r, piv_mark);   // (+ row r recorded)
+    SX_PROBE(8 + 10 * t);
+    best = cluster_min(best, slot, ph, nullptr, 0, false, &sh_r[t], r, piv_mark,   // (+ row r recorded)
+                       prb ? prb + 9 + 10 * t : nullptr);
     ph ^= 1;
-    SX_PROBE(5 + 4 * t);
+    SX_PROBE(11 + 10 * t);
   }
 #undef SX_PROBE
+#undef SX_PROBE_DEP
+  if (gtid == 0) {
+    st->status = status;
+    st->it = it;
+    st->sb[bown] = t;
+    st->go = t > 0;
+    st->pend_r = -1;
+  }
+}
+
+// ------------------------------------------------------------------ k_look2
+// k_look2: k_lookahead's selection (same pivots, same arithmetic, same order: bitwise identical)
+// reorganised so that a pivot's two phases are short.  ncu of k_lookahead showed
+// the selection issue- and dependency-bound: each phase re-read up to 31 chain operands per
+// element through L2 (the cluster barrier's acquire invalidates L1), every thread re-loaded up to
+// 33 broadcast scalars, and the chains carried a bit-test + two selects per operand.  Here:
+//   * the previous bank's chain operands of a thread's elements (PS) live in SHARED memory as
+//     double2 pairs [q][u/2][tid] (one conflict-free LDS.128 per two operands), copied in at
+//     launch start from the global hand-off s.hand[bpre], which the previous launch wrote from the
+//     SAME thread positions; the own bank (this launch's pivots: col_u[i] of its rows, prow_u[j]
+//     of its columns) lives in shared memory too when it fits (OS), else in the hand-off slots
+//     s.hand[bown] themselves (own writes read back through L2, every load of a phase in flight
+//     at once);
+//   * the running objective row R0 and rhs column RHS of own elements stay in shared memory;
+//   * a phase's broadcast operands (prow_u[k] of both banks + the previous pivot's rhs entry;
+//     col_u[r] of both banks + col_t[0]) are loaded ONCE per warp, one lane per value, behind the
+//     phase's own T loads, into a per-warp shared buffer read with broadcast LDS.128;
+//   * QC / QR own columns / rows per thread are compile-time, so their chains interleave
+//     (instruction-level parallelism on the 8-cycle DFMA dependency), and the common case — the
+//     pivot row of this step is no pending pivot row, the previous bank is full — runs plain FMA
+//     chains without per-operand selects or predicates;
+//   * chunks of 32 consecutive elements are dealt to the cluster's CTAs round-robin, so small
+//     tableaux keep every SM of the cluster busy.
+// The pass (k_update_s) still gets colS / prowS from global memory.
+template <int NT, bool PS, bool OS, int QC, int QR>
+__global__ void __launch_bounds__(NT, 1) k_look2(SlabView s, const double* __restrict__ T, int S, int bown,
+                                                 int bpre, int nqc, int nqr, double tol_opt, double tol_piv) {
+  pdl_launch_dependents();                            // the previous block's pass may start now
+  cluster_arrive_relaxed();                           // (waited for in the first cluster_min)
+  constexpr int NW = NT / 32;
+  constexpr int H = kMaxLook / 2;                     // operand pairs per bank
+  DevState* st = s.st;
+  __shared__ int sh_r[kMaxLook];
+  __shared__ int sh_rp[kMaxLook];
+  __shared__ __align__(16) Cand slot[2 * 16];
+  __shared__ __align__(16) double bcw[NW][36];       // per-warp broadcast operands of a phase
+  extern __shared__ __align__(16) unsigned int sm2[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = (int)gridDim.x * NT;
+  const int gtid = (int)blockIdx.x * NT + tid;
+  const int rows = s.rows;
+  const long long ld = s.ld;
+  const int w = s.w;
+  const int pw = st->pw;
+  const int mwords = ((rows + 31) / 32 + 3) & ~3;
+  unsigned int* piv_mark = sm2;
+  double2* OP = reinterpret_cast<double2*>(sm2 + mwords);          // OS: [QC][H][NT] own prow_u[j]
+  double2* OC = OP + (OS ? (size_t)QC * H * NT : 0);                // OS: [QR][H][NT] own col_u[i]
+  double* R0s = reinterpret_cast<double*>(OC + (OS ? (size_t)QR * H * NT : 0));   // [QC][NT]
+  double* RHSs = R0s + (size_t)QC * NT;                                          // [QR][NT]
+  double2* PPs = reinterpret_cast<double2*>(RHSs + (size_t)QR * NT);    // PS: [QC][H][NT]
+  double2* PCs = PPs + (size_t)QC * H * NT;                              // PS: [QR][H][NT]
+  const size_t hbank = (size_t)(nqc + nqr) * H * G;  // hand-off: [nqc][H][G] columns, [nqr][H][G] rows
+  double2* __restrict__ hown = s.hand + (size_t)bown * hbank;
+  const double2* __restrict__ hpre = s.hand + (size_t)(bpre >= 0 ? bpre : 0) * hbank;
+  double* __restrict__ colO = s.colS + bown * kMaxLook;
+  const double* __restrict__ colP = s.colS + (bpre >= 0 ? bpre : 0) * kMaxLook;
+  double* __restrict__ prowO = s.prowS + (long long)bown * kMaxLook * ld;
+  const double* __restrict__ prowP = s.prowS + (long long)(bpre >= 0 ? bpre : 0) * kMaxLook * ld;
+  long long it = st->it;
+  int status = st->status;
+  const long long stop = st->stop_at;
+  const long long cap = st->cap;
+  const int spre = bpre >= 0 ? st->sb[bpre] : 0;
+  int ph = 0;
+  // own columns / rows (valid: < ld / < rows): element e = lane + 32 (cta + C (warp + NW q))
+  const int C = (int)gridDim.x;
+  long long jq[QC], iq[QR];
+#pragma unroll
+  for (int q = 0; q < QC; ++q) jq[q] = lane + 32LL * (blockIdx.x + (long long)C * (wid + (long long)NW * q));
+#pragma unroll
+  for (int q = 0; q < QR; ++q) iq[q] = lane + 32LL * (blockIdx.x + (long long)C * (wid + (long long)NW * q));
+  unsigned long long* prb = s.probe ? s.probe + ((size_t)((it / kMaxLook) % kProbeSlots) * 16 + (blockIdx.x & 15)) * kProbeEv
+                                    : nullptr;
+#ifdef SX_PROBE_DETAIL
+#define SX_TIMER "%%clock64"                          // detail probes: SM cycles (intervals within a CTA)
+#else
+#define SX_TIMER "%%globaltimer"
+#endif
+#define SX_PROBE(e)                                                                 \
+  do {                                                                              \
+    if (prb && threadIdx.x == 0) {                                                  \
+      unsigned long long tnow;                                                      \
+      asm volatile("mov.u64 %0, " SX_TIMER ";" : "=l"(tnow));                       \
+      prb[e] = tnow;                                                                \
+    }                                                                               \
+  } while (0)
+  SX_PROBE(0);
+  // chain operand pair v of own column / row q: previous bank (smem copy, or the hand-off, read
+  // only for valid elements) and own bank (smem, or this launch's hand-off slots)
+  auto pre_c = [&](int q, int v) -> double2 {
+    if (PS) return PPs[((size_t)q * H + v) * NT + tid];
+    return jq[q] < ld ? __ldg(hpre + ((size_t)q * H + v) * G + gtid) : make_double2(0.0, 0.0);
+  };
+  auto pre_r = [&](int q, int v) -> double2 {
+    if (PS) return PCs[((size_t)q * H + v) * NT + tid];
+    return iq[q] < rows ? __ldg(hpre + ((size_t)(nqc + q) * H + v) * G + gtid) : make_double2(0.0, 0.0);
+  };
+  auto own_c = [&](int q, int v) -> double2 {
+    if (OS) return OP[((size_t)q * H + v) * NT + tid];
+    return jq[q] < ld ? __ldcg(hown + ((size_t)q * H + v) * G + gtid) : make_double2(0.0, 0.0);
+  };
+  auto own_r = [&](int q, int v) -> double2 {
+    if (OS) return OC[((size_t)q * H + v) * NT + tid];
+    return iq[q] < rows ? __ldcg(hown + ((size_t)(nqc + q) * H + v) * G + gtid) : make_double2(0.0, 0.0);
+  };
+  auto own_c_set = [&](int q, int u, double val) {
+    if (OS) reinterpret_cast<double*>(OP + ((size_t)q * H + (u >> 1)) * NT + tid)[u & 1] = val;
+    else reinterpret_cast<double*>(hown + ((size_t)q * H + (u >> 1)) * G + gtid)[u & 1] = val;
+  };
+  auto own_r_set = [&](int q, int u, double val) {
+    if (OS) reinterpret_cast<double*>(OC + ((size_t)q * H + (u >> 1)) * NT + tid)[u & 1] = val;
+    else reinterpret_cast<double*>(hown + ((size_t)(nqc + q) * H + (u >> 1)) * G + gtid)[u & 1] = val;
+  };
+  const int vpre = (spre + 1) >> 1;                   // pairs holding the spre previous operands
+  if (PS && spre > 0) {
+#pragma unroll
+    for (int q = 0; q < QC; ++q)
+      if (jq[q] < ld)
+        for (int v = 0; v < vpre; ++v)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(PPs + ((size_t)q * H + v) * NT + tid)),
+                       "l"(hpre + ((size_t)q * H + v) * G + gtid)
+                       : "memory");
+#pragma unroll
+    for (int q = 0; q < QR; ++q)
+      if (iq[q] < rows)
+        for (int v = 0; v < vpre; ++v)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(PCs + ((size_t)q * H + v) * NT + tid)),
+                       "l"(hpre + ((size_t)(nqc + q) * H + v) * G + gtid)
+                       : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int q = tid; q < (rows + 31) / 32; q += NT) piv_mark[q] = 0u;
+  if (tid < kMaxLook) sh_rp[tid] = tid < spre ? st->rsb[bpre][tid] : -1;
+  Cand best = cand_none();
+#pragma unroll
+  for (int q = 0; q < QC; ++q) {
+    const long long j = jq[q];
+    if (j < ld) {
+      const double v = bpre < 0 ? T[j] : s.R0[j];
+      R0s[q * NT + tid] = v;
+      if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < QR; ++q)
+    if (iq[q] < rows) RHSs[q * NT + tid] = bpre < 0 ? T[iq[q] * ld + w] : s.RHS[iq[q]];
+  __syncthreads();
+  if (tid < spre) atomicOr(&piv_mark[sh_rp[tid] >> 5], 1u << (sh_rp[tid] & 31));
+  best = cluster_min(best, slot, ph, nullptr, 0, true);   // (its barriers also publish piv_mark)
+  ph ^= 1;
+  SX_PROBE(1);
+  if (PS && spre > 0) asm volatile("cp.async.wait_group 0;" ::: "memory");   // own entries only: no barrier
+
+  int t = 0;
+  int r_prev = spre > 0 ? sh_rp[spre - 1] : -1;       // pivot not yet applied to RHS
+  const double* p_prev = spre > 0 ? prowP + (long long)(spre - 1) * ld : nullptr;
+  double* bw = bcw[wid];
+  const double2* bw2 = reinterpret_cast<const double2*>(bw);
+  for (; t < S; ++t) {
+    if (status != kRunning || it >= stop) break;
+    if (best.idx == LLONG_MAX) { status = kOptimal; break; }                 // Step 1: optimal
+    const long long k = best.idx - s.c0;
+    // ---- phase A: rows.  Own T entries first (HBM), then the warp's broadcast operands.
+    double x[QR];
+#pragma unroll
+    for (int q = 0; q < QR; ++q) x[q] = iq[q] < rows ? T[iq[q] * ld + k] : 0.0;
+    {                                                  // lane u: prow_u[k] (prev bank u < 16, own 16+u)
+      const int u = lane & (kMaxLook - 1);             // (own bank: written before the last barrier)
+      const bool ok = lane < kMaxLook ? u < spre : u < t;
+      const double* src = (lane < kMaxLook ? prowP : prowO) + (long long)u * ld + k;
+      const double v = ok ? *src : 0.0;
+      const double v2 = lane == 0 && r_prev >= 0 ? p_prev[w] : 0.0;   // both loads in flight at once
+      bw[lane] = v;
+      if (lane == 0) bw[32] = v2;
+      __syncwarp();
+    }
+    SX_PROBE(2 + 10 * t);
+    // own-bank operands of the own rows, every load in flight at once (OS: shared memory)
+    double2 ob[QR][H];
+#pragma unroll
+    for (int v = 0; v < H; ++v)
+#pragma unroll
+      for (int q = 0; q < QR; ++q) ob[q][v] = 2 * v < t ? own_r(q, v) : make_double2(0.0, 0.0);
+    const double pw_prev = bw[32];
+    double h[QR];
+    bool marked = false;
+#pragma unroll
+    for (int q = 0; q < QR; ++q) {
+      const long long i = iq[q];
+      h[q] = RHSs[q * NT + tid];
+      if (r_prev >= 0) {
+        double cpv;
+        if (t > 0) {
+          cpv = 0.0;
+#pragma unroll
+          for (int v = 0; v < H; ++v)
+            if (v == ((t - 1) >> 1)) cpv = ((t - 1) & 1) ? ob[q][v].y : ob[q][v].x;
+        } else {
+          cpv = PS ? reinterpret_cast<const double*>(PCs + ((size_t)q * H + ((spre - 1) >> 1)) * NT + tid)[(spre - 1) & 1]
+                   : (i < rows ? reinterpret_cast<const double*>(hpre + ((size_t)(nqc + q) * H + ((spre - 1) >> 1)) * G + gtid)[(spre - 1) & 1]
+                               : 0.0);
+        }
+        h[q] = (i == r_prev) ? pw_prev : __fma_rn(-cpv, pw_prev, h[q]);
+        if (i < rows) RHSs[q * NT + tid] = h[q];
+      }
+      if (i < rows && ((piv_mark[i >> 5] >> (i & 31)) & 1u)) marked = true;
+    }
+#ifdef SX_PROBE_DETAIL
+    SX_PROBE(3 + 10 * t);
+#endif
+    if (!marked) {                                     // no own row is a pending pivot row: plain chains
+#pragma unroll
+      for (int v = 0; v < H; ++v) {
+        if (spre < kMaxLook && 2 * v >= spre) break;
+        const double2 bq = bw2[v];                     // qk pair (broadcast LDS)
+        double2 a[QR];
+#pragma unroll
+        for (int q = 0; q < QR; ++q) a[q] = pre_r(q, v);
+#pragma unroll
+        for (int q = 0; q < QR; ++q) {
+          x[q] = __fma_rn(-a[q].x, bq.x, x[q]);
+          if (spre == kMaxLook || 2 * v + 1 < spre) x[q] = __fma_rn(-a[q].y, bq.y, x[q]);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < H; ++v) {
+        if (2 * v >= t) break;
+        const double2 bp = bw2[H + v];                 // pk pair
+#pragma unroll
+        for (int q = 0; q < QR; ++q) {
+          x[q] = __fma_rn(-ob[q][v].x, bp.x, x[q]);
+          if (2 * v + 1 < t) x[q] = __fma_rn(-ob[q][v].y, bp.y, x[q]);
+        }
+      }
+    } else {                                           // some own row was a pivot row: take prow there
+#pragma unroll
+      for (int q = 0; q < QR; ++q) {
+        const long long i = iq[q];
+#pragma unroll
+        for (int v = 0; v < H; ++v) {
+          const double2 bq = bw2[v];
+          const double2 a = 2 * v < spre ? pre_r(q, v) : make_double2(0.0, 0.0);
+          if (2 * v < spre) x[q] = (i == sh_rp[2 * v]) ? bq.x : __fma_rn(-a.x, bq.x, x[q]);
+          if (2 * v + 1 < spre) x[q] = (i == sh_rp[2 * v + 1]) ? bq.y : __fma_rn(-a.y, bq.y, x[q]);
+        }
+#pragma unroll
+        for (int v = 0; v < H; ++v) {
+          const double2 bp = bw2[H + v];
+          if (2 * v < t) x[q] = (i == sh_r[2 * v]) ? bp.x : __fma_rn(-ob[q][v].x, bp.x, x[q]);
+          if (2 * v + 1 < t) x[q] = (i == sh_r[2 * v + 1]) ? bp.y : __fma_rn(-ob[q][v].y, bp.y, x[q]);
+        }
+      }
+    }
+#ifdef SX_PROBE_DETAIL
+    SX_PROBE(4 + 10 * t);
+#endif
+    Cand rb = cand_none();
+#pragma unroll
+    for (int q = 0; q < QR; ++q) {
+      const long long i = iq[q];
+      if (i < rows) {
+        own_r_set(q, t, x[q]);
+        colO[i * kColS + t] = x[q];                    // (row-major: the pass's TMA rows)
+        if (i >= 1 && x[q] > tol_piv)                                           // Step 2
+          rb = cand_min(rb, ratio_cand(s.rule, __ddiv_rn(h[q], x[q]), i, s.rule ? __ldcg(s.basis + i - 1) : 0));
+      }
+    }
+#ifdef SX_PROBE_DETAIL
+    SX_PROBE(5 + 10 * t);
+    rb = cluster_min(rb, slot, ph, T, ld);
+#else
+    SX_PROBE(3 + 10 * t);
+    rb = cluster_min(rb, slot, ph, T, ld, false, nullptr, 0, nullptr, prb ? prb + 4 + 10 * t : nullptr);
+#endif
+    ph ^= 1;
+    SX_PROBE(6 + 10 * t);
+    if (rb.idx == LLONG_MAX) {                                                 // unbounded
+      status = kUnbounded;
+      if (gtid == 0) st->k = (int)(k + s.c0);
+      break;
+    }
+    if (it >= cap) { status = kIterLimit; break; }                            // reading c12
+    const int r = cand_row(rb.idx);
+    // ---- phase B: columns.  Own entries of row r first (L2: prefetched during reduction A).
+    const double* Tr = T + (long long)r * ld;
+    double y[QC];
+#pragma unroll
+    for (int q = 0; q < QC; ++q) y[q] = jq[q] < ld ? Tr[jq[q]] : 0.0;
+    {                                                  // lane u: col_u[r] (prev bank u < 16, own 16+u, u <= t)
+      const int u = lane & (kMaxLook - 1);
+      const bool ok = lane < kMaxLook ? u < spre : u <= t;
+      const double* src = (lane < kMaxLook ? colP : colO) + (long long)r * kColS + u;
+      const double v = ok ? *src : 0.0;
+      const double v2 = lane == 0 ? -colO[t] : 0.0;                // -col_t[0]
+      bw[lane] = v;
+      if (lane == 0) bw[32] = v2;
+      __syncwarp();
+    }
+    double2 ob2[QC][H];                                // own-bank operands of the own columns
+#pragma unroll
+    for (int v = 0; v < H; ++v)
+#pragma unroll
+      for (int q = 0; q < QC; ++q) ob2[q][v] = 2 * v < t ? own_c(q, v) : make_double2(0.0, 0.0);
+    const double p = bw[kMaxLook + t];
+    const double a0 = bw[32];
+    SX_PROBE(7 + 10 * t);
+    double* prow = prowO + (long long)t * ld;
+    unsigned int rmask = 0u, qmask = 0u;                // bit u: r was pivot row u (own / previous bank)
+#pragma unroll
+    for (int u = 0; u < kMaxLook; ++u) {
+      if (u < t && sh_r[u] == r) rmask |= 1u << u;
+      if (u < spre && sh_rp[u] == r) qmask |= 1u << u;
+    }
+    if ((rmask | qmask) == 0u) {                        // row r is no pending pivot row: plain chains
+#pragma unroll
+      for (int v = 0; v < H; ++v) {
+        if (spre < kMaxLook && 2 * v >= spre) break;
+        const double2 cs = bw2[v];
+        double2 a[QC];
+#pragma unroll
+        for (int q = 0; q < QC; ++q) a[q] = pre_c(q, v);
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          y[q] = __fma_rn(-cs.x, a[q].x, y[q]);
+          if (spre == kMaxLook || 2 * v + 1 < spre) y[q] = __fma_rn(-cs.y, a[q].y, y[q]);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < H; ++v) {
+        if (2 * v >= t) break;
+        const double2 cr = bw2[H + v];
+#pragma unroll
+        for (int q = 0; q < QC; ++q) {
+          y[q] = __fma_rn(-cr.x, ob2[q][v].x, y[q]);
+          if (2 * v + 1 < t) y[q] = __fma_rn(-cr.y, ob2[q][v].y, y[q]);
+        }
+      }
+    } else {                                           // row r was a pivot row u: prow_u replaces it
+#pragma unroll
+      for (int q = 0; q < QC; ++q) {
+#pragma unroll
+        for (int v = 0; v < H; ++v) {
+          const double2 cs = bw2[v];
+          const double2 a = 2 * v < spre ? pre_c(q, v) : make_double2(0.0, 0.0);
+          if (2 * v < spre) y[q] = ((qmask >> (2 * v)) & 1u) ? a.x : __fma_rn(-cs.x, a.x, y[q]);
+          if (2 * v + 1 < spre) y[q] = ((qmask >> (2 * v + 1)) & 1u) ? a.y : __fma_rn(-cs.y, a.y, y[q]);
+        }
+#pragma unroll
+        for (int v = 0; v < H; ++v) {
+          const double2 cr = bw2[H + v];
+          if (2 * v < t) y[q] = ((rmask >> (2 * v)) & 1u) ? ob2[q][v].x : __fma_rn(-cr.x, ob2[q][v].x, y[q]);
+          if (2 * v + 1 < t) y[q] = ((rmask >> (2 * v + 1)) & 1u) ? ob2[q][v].y : __fma_rn(-cr.y, ob2[q][v].y, y[q]);
+        }
+      }
+    }
+#ifdef SX_PROBE_DETAIL
+    SX_PROBE(8 + 10 * t);
+#endif
+    best = cand_none();
+#pragma unroll
+    for (int q = 0; q < QC; ++q) {
+      const long long j = jq[q];
+      if (j < ld) {
+        const double pj = __ddiv_rn(y[q], p);
+        own_c_set(q, t, pj);
+        prow[j] = pj;
+        const double v = __fma_rn(a0, pj, R0s[q * NT + tid]);
+        R0s[q * NT + tid] = v;
+        if (j < pw && v < -tol_opt) best = cand_min(best, price_cand(s.rule, v, s.c0 + j));  // Step 1 of t+1
+      }
+    }
+    if (gtid == 0) {
+      st->rsb[bown][t] = r;
+      s.basis[r - 1] = (int)(k + s.c0);
+      if (it < s.trace_cap) {
+        s.trace_k[it] = (int)(k + s.c0);
+        s.trace_r[it] = r;
+      }
+    }
+    ++it;
+    r_prev = r;
+    p_prev = prow;
+#ifdef SX_PROBE_DETAIL
+    SX_PROBE(9 + 10 * t);
+    best = cluster_min(best, slot, ph, nullptr, 0, false, &sh_r[t], r, piv_mark);   // (+ row r recorded)
+    SX_PROBE(10 + 10 * t);
+#else
+    SX_PROBE(8 + 10 * t);
+    best = cluster_min(best, slot, ph, nullptr, 0, false, &sh_r[t], r, piv_mark,   // (+ row r recorded)
+                       prb ? prb + 9 + 10 * t : nullptr);
+#endif
+    ph ^= 1;
+    SX_PROBE(11 + 10 * t);
+  }
+#undef SX_PROBE
+#undef SX_TIMER
+  // hand-off: own R0 / RHS back to global; OS: the own bank's operands to s.hand[bown] (the next
+  // launch's previous bank, read by the same thread positions; without OS they are already there)
+  const int vown = (t + 1) >> 1;
+#pragma unroll
+  for (int q = 0; q < QC; ++q) {
+    if (jq[q] < ld) {
+      s.R0[jq[q]] = R0s[q * NT + tid];
+      if (OS)
+        for (int v = 0; v < vown; ++v) hown[((size_t)q * H + v) * G + gtid] = OP[((size_t)q * H + v) * NT + tid];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < QR; ++q) {
+    if (iq[q] < rows) {
+      s.RHS[iq[q]] = RHSs[q * NT + tid];
+      if (OS)
+        for (int v = 0; v < vown; ++v)
+          hown[((size_t)(nqc + q) * H + v) * G + gtid] = OC[((size_t)q * H + v) * NT + tid];
+    }
+  }
   if (gtid == 0) {
     st->status = status;
     st->it = it;
@@ -1955,8 +2404,93 @@ size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int*
   return mark;
 }
 
+// k_look2 instantiations: (own columns QC, own rows QR per thread, own bank in shared memory OS);
+// a slab takes the first that covers its (nqc, nqr) and fits in shared memory WITH the previous
+// bank (the pipelined launches), else k_lookahead.  Measured (round 3, pipelined blocks): 1000^2
+// 110-118 us (k_lookahead ~135), 2000^2 115-121 (134), 4000^2 157-166 (166); with the own bank in
+// the hand-off slots (OS = 0, the only way 8000^2 fits) 388 us against k_lookahead's 343 — so the
+// OS = 0 configurations are not offered and 8000^2 and larger keep k_lookahead.
+static const int kLook2Q[][3] = {{1, 1, 1}, {2, 1, 1}};   // (ld >= rows: QR <= QC always)
+constexpr int kLook2NQ = sizeof(kLook2Q) / sizeof(kLook2Q[0]);
+
+size_t look2_smem(const SlabView& s, int nt, bool ps, bool os, int qc, int qr) {
+  const size_t mark = (size_t)(((s.rows + 31) / 32 + 3) & ~3) * sizeof(unsigned int);
+  const size_t q = (size_t)(qc + qr), bank = q * nt * (kMaxLook / 2) * sizeof(double2);
+  return mark + q * nt * sizeof(double) + (os ? bank : 0) + (ps ? bank : 0);
+}
+
+template <bool PS, bool OS, int QC, int QR>
+static cudaError_t look2_attr(int cluster, int* nclusters) {
+  auto kern = k_look2<256, PS, OS, QC, QR>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLook2SmemMax);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, kLook2SmemMax, nullptr, attr);
+  cfg.blockDim = dim3(256);
+  return cudaOccupancyMaxActiveClusters(nclusters, kern, &cfg);
+}
+
+template <bool PS>
+static cudaError_t look2_attr_q(int qi, int cluster, int* n) {
+  switch (qi) {
+    case 0: return look2_attr<PS, true, 1, 1>(cluster, n);
+    default: return look2_attr<PS, true, 2, 1>(cluster, n);
+  }
+}
+
+long long look2_prepare(SlabView* s, int cluster) {
+  const int nt = 256;
+  const long long G = (long long)cluster * nt;
+  const int nqc = (int)((s->ld + G - 1) / G), nqr = (int)((s->rows + G - 1) / G);
+  for (int qi = 0; qi < kLook2NQ; ++qi) {
+    const int qc = kLook2Q[qi][0], qr = kLook2Q[qi][1], os = kLook2Q[qi][2];
+    if (qc < nqc || qr < nqr || look2_smem(*s, nt, true, os, qc, qr) > kLook2SmemMax) continue;
+    int n0 = 0, n1 = 0;
+    cudaError_t e = look2_attr_q<false>(qi, cluster, &n0);
+    if (e == cudaSuccess) e = look2_attr_q<true>(qi, cluster, &n1);
+    if (e != cudaSuccess || n0 < 1 || n1 < 1) {
+      cudaGetLastError();
+      return 0;
+    }
+    s->look_nt = nt;
+    s->look_qc = qc;
+    s->look_qr = qr;
+    s->look_os = os;
+    s->look_nqc = nqc;
+    s->look_nqr = nqr;
+    return 2LL * (nqc + nqr) * (kMaxLook / 2) * G;   // hand-off double2 entries (two banks)
+  }
+  return 0;
+}
+
+template <bool PS, bool OS, int QC, int QR>
+static cudaError_t look2_launch(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
+                                double tol_piv, int cluster, cudaStream_t st) {
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, look2_smem(s, 256, PS, OS, QC, QR), st, attr);
+  cfg.blockDim = dim3(256);
+  return cudaLaunchKernelEx(&cfg, k_look2<256, PS, OS, QC, QR>, s, T, S, bown, bpre, s.look_nqc, s.look_nqr,
+                            tol_opt, tol_piv);
+}
+
+template <bool PS>
+static cudaError_t look2_launch_q(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
+                                  double tol_piv, int cluster, cudaStream_t st) {
+  const int qc = s.look_qc, qr = s.look_qr;
+  if (qc == 1 && qr == 1) return look2_launch<PS, true, 1, 1>(s, T, S, bown, bpre, tol_opt, tol_piv, cluster, st);
+  return look2_launch<PS, true, 2, 1>(s, T, S, bown, bpre, tol_opt, tol_piv, cluster, st);
+}
+
 cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
                              double tol_piv, int cluster, bool cache, cudaStream_t st) {
+  if (s.look_nt > 0) {
+    // the previous bank in shared memory (always fits: look2_prepare), read from the hand-off only
+    // when the caller disables the cache (experiments)
+    const bool ps = cache && bpre >= 0;
+    return ps ? look2_launch_q<true>(s, T, S, bown, bpre, tol_opt, tol_piv, cluster, st)
+              : look2_launch_q<false>(s, T, S, bown, bpre, tol_opt, tol_piv, cluster, st);
+  }
   int nqc = 0, nqr = 0;
   const size_t smem = lookahead_smem(s, cluster, cache && bpre >= 0, &nqc, &nqr);
   cudaLaunchAttribute attr[1];

@@ -40,6 +40,13 @@ constexpr size_t kLookCacheMax = 200 * 1024;
 cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
                              double tol_piv, int cluster, bool cache, cudaStream_t st);
 size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int* nqr);
+// k_look2 (the default single-part selection when its own-bank operands fit in shared memory):
+// own column / row slots per thread and the dynamic shared memory (ps: previous bank too)
+constexpr size_t kLook2SmemMax = 220 * 1024;
+size_t look2_smem(const SlabView& s, int nt, bool ps, bool os, int qc, int qr);
+// picks the k_look2 instantiation for the slab (s->look_*) and sets the kernel attributes; returns
+// the hand-off size in double2 entries, 0 if k_look2 does not fit (the slab keeps k_lookahead)
+long long look2_prepare(SlabView* s, int cluster);
 // k_mlook: one pivot t (t = -1: block start) of the multi-part look-ahead, between two exchanges
 // xp.n > 0: the slot goes to every rank's gather buffer over peer memory + flags (no NCCL)
 cudaError_t launch_mlook(const SlabView& s, const double* xin, double* xout, int nparts, long long xstride, int t,

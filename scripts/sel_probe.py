@@ -29,11 +29,14 @@ Ad, bd, cd = (torch.from_numpy(v).cuda() for v in (A, b, c))
 with sx.Simplex(Ad, bd, cd, overlap=not serial) as s:
     s.iterate(piv)
     torch.cuda.synchronize()
-K, EV = 16, 2 + 4 * 16
+K, NE = 16, 10
+EV = 2 + NE * K
 P = np.fromfile(path, dtype=np.uint64).reshape(64, 16, EV).astype(np.float64)
 ok = (P > 0).all(axis=(1, 2)) & (np.diff(P, axis=2) >= 0).all(axis=(1, 2))
 ok &= (P[:, :, EV - 1] - P[:, :, 0] < 5e6).all(axis=1)
 P = P[ok]                                   # complete launches, stamps of one launch only
+if os.environ.get("SIMPLEX_PROBE_DETAIL"):
+    P = P * 1e3 / float(os.environ.get("SIMPLEX_PROBE_MHZ", "1965"))   # cycles -> ns
 print(f"{len(P)} complete launches ({'serial' if serial else 'pipelined'}), {m}x{n}")
 t0 = P[:, :, 0:1]
 tot = (P[:, :, EV - 1] - P[:, :, 0]) / 1e3
@@ -41,11 +44,16 @@ print(f"launch: {tot.mean():.1f} us (CTA min {tot.min(axis=1).mean():.1f} max {t
 pro = (P[:, :, 1] - P[:, :, 0]) / 1e3
 print(f"prologue (cache fill + first pricing + reduction): {pro.mean():.2f} us")
 prev = P[:, :, 1]
-names = ["phase A (rows)", "reduction A", "phase B (cols)", "reduction B"]
+names = ["A: loads arrive", "A: chain+ratio", "redA: CTA", "redA: cl.barrier", "redA: fold",
+         "B: loads arrive", "B: chain+price", "redB: CTA", "redB: cl.barrier", "redB: fold"]
+if os.environ.get("SIMPLEX_PROBE_DETAIL"):      # library built with -DSX_PROBE_DETAIL (k_look2 only)
+    names = ["A: loads arrive", "A: rhs+mark", "A: chains", "A: store+div", "redA (all)",
+             "B: loads arrive", "B: chains", "B: div+R0+cand", "redB (all)", "(none)"]
+    # stamps are SM clock64 cycles: report us at the SM clock given (MHz), default 1965
 acc = {nm: [] for nm in names}
 for t in range(K):
     for q, nm in enumerate(names):
-        cur = P[:, :, 2 + 4 * t + q]
+        cur = P[:, :, 2 + NE * t + q]
         acc[nm].append((cur - prev) / 1e3)
         prev = cur
 for nm in names:

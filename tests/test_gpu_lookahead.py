@@ -262,3 +262,22 @@ def test_multipart_golden_1000(sx):
     assert np.array_equal(k, g["trace_k"]) and np.array_equal(r, g["trace_r"])
     assert obj == float(g["objective"]) and np.array_equal(y, g["y"])
     assert h == int(g["tableau_hash"])
+
+
+# Which selection kernel a handle runs (stats.path): k_look2, the shared-memory selection
+# (path 3), when one column part has m + 1 <= 4096 rows and a pitch <= 8192
+# doubles; k_lookahead (path 0) beyond.  Both must be bitwise the oracle's pivots on each side of
+# the boundary, with the cluster's round-robin 32-element chunks ending raggedly.
+_ORACLE_120 = {}
+
+
+@pytest.mark.parametrize("m,n,want", [(1000, 1000, 3), (2000, 2000, 3), (4095, 300, 3), (4096, 200, 0),
+                                      (4100, 300, 0), (3000, 5300, 0), (77, 4000, 3)])
+def test_selection_kernel_choice(sx, m, n, want, ov):
+    A, b, c = lpgen.dense_lp(m, n, 7)
+    if (m, n) not in _ORACLE_120:
+        _ORACLE_120[(m, n)] = oracle.solve(A, b, c, max_pivots=120, keep_tableau=True)
+    o = _ORACLE_120[(m, n)]
+    with sx.Simplex(A, b, c, max_pivots=120, overlap=ov) as s:
+        assert s.stats().path == want
+    assert_same(gpu_solve(sx, A, b, c, max_pivots=120, lookahead=0, overlap=ov), o)
