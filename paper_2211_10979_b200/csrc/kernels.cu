@@ -677,6 +677,8 @@ __global__ void __launch_bounds__(kThreads) k_update(SlabView s, int q, double t
 #define SX_LDP(p) __ldg(p)
 #endif
 constexpr int kLookRB = SX_LOOK_RB;                 // rows per load batch of a selection thread
+constexpr int kLookPreT = 2;                        // rows whose T entry is requested up front
+constexpr int kLookPreC = 4;                        // columns whose row-r entry is requested up front
 constexpr int kLookCB = SX_LOOK_CB;                 // columns per load batch
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -897,13 +899,29 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     Cand rb = cand_none();
     // rows in batches of kLookRB per thread: every load of the batch (the T entry, the rhs, the
     // chain operands) is issued before the first dependent FMA, so a batch costs one latency
+    // the entering column's entries of this thread's first kLookPreT rows are requested at once
+    // (HBM), so the row batches below do not each wait for their own HBM round trip
+    double tpre[kLookPreT];
+#pragma unroll
+    for (int b = 0; b < kLookPreT; ++b) {
+      const long long i = gtid + (long long)b * gthreads;
+      tpre[b] = i < rows ? T[i * ld + k] : 0.0;
+    }
     for (long long i0 = gtid, qi0 = 0; i0 < rows; i0 += kLookRB * gthreads, qi0 += kLookRB) {
       double xb[kLookRB], hb[kLookRB], cpb[kLookRB], cub[kLookRB][kMaxLook];
 #pragma unroll
       for (int b = 0; b < kLookRB; ++b) {
         const long long i = i0 + b * gthreads;
         const bool v = b == 0 || i < rows;
-        xb[b] = v ? T[i * ld + k] : 0.0;
+        double xv = 0.0;
+        bool have = false;
+#pragma unroll
+        for (int pb = 0; pb < kLookPreT; ++pb)
+          if (qi0 + b == pb) {
+            xv = tpre[pb];
+            have = true;
+          }
+        xb[b] = have ? xv : (v ? T[i * ld + k] : 0.0);
         hb[b] = v ? RHS[i] : 0.0;
         cpb[b] = v && r_prev >= 0 ? c_prev[i] : 0.0;
 #pragma unroll
@@ -974,13 +992,27 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
     }
     best = cand_none();
     // columns in batches of kLookCB per thread (loads of the batch first, as for the rows)
+    double rpre[kLookPreC];                             // row r's entries of the first columns, at once
+#pragma unroll
+    for (int b = 0; b < kLookPreC; ++b) {
+      const long long j = gtid + (long long)b * gthreads;
+      rpre[b] = j < ld ? Tr[j] : 0.0;
+    }
     for (long long j0 = gtid, qj0 = 0; j0 < ld; j0 += kLookCB * gthreads, qj0 += kLookCB) {
       double xb[kLookCB], r0b[kLookCB], pub[kLookCB][kMaxLook];
 #pragma unroll
       for (int b = 0; b < kLookCB; ++b) {
         const long long j = j0 + b * gthreads;
         const bool v = b == 0 || j < ld;
-        xb[b] = v ? Tr[j] : 0.0;
+        double xv = 0.0;
+        bool have = false;
+#pragma unroll
+        for (int pb = 0; pb < kLookPreC; ++pb)
+          if (qj0 + b == pb) {
+            xv = rpre[pb];
+            have = true;
+          }
+        xb[b] = have ? xv : (v ? Tr[j] : 0.0);
         r0b[b] = v ? R0[j] : 0.0;
 #pragma unroll
         for (int u = 0; u < kMaxLook; ++u) pub[b][u] = v && u < t ? prowO[(long long)u * ld + j] : 0.0;
