@@ -503,6 +503,9 @@ def main():
         torch.cuda.synchronize()
 
     def one_step(reload=True):
+        if reload and small:                                 # one call, one launch, one sync
+            _, _, obj, piv, status = solver.solve_lp(dA, db, dc, dx, dy)
+            return status, obj, piv
         if reload:
             solver.reset(dA, db, dc)
         status = solver.solve()
@@ -671,13 +674,21 @@ def main():
     yh_out = np.empty(m)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_reps = args.steps if small else 1                     # a 64^2 solve is ~0.1 ms: average K calls
+    if small:
+        solver.solve_lp(Ah, bh, ch, xh_out, yh_out)           # (untimed warm-up of the host-input path)
+        barrier()
     e0.record()
-    solver.reset(Ah, bh, ch)
-    solver.solve()
-    _, _, obj_e2e, piv_e2e, _ = solver.solution(xh_out, yh_out)
+    if small:
+        for _ in range(e2e_reps):
+            _, _, obj_e2e, piv_e2e, _ = solver.solve_lp(Ah, bh, ch, xh_out, yh_out)
+    else:
+        solver.reset(Ah, bh, ch)
+        solver.solve()
+        _, _, obj_e2e, piv_e2e, _ = solver.solution(xh_out, yh_out)
     e1.record()
     barrier()
-    e2e_ms = e0.elapsed_time(e1)
+    e2e_ms = e0.elapsed_time(e1) / e2e_reps
     if world > 1:
         e2e_ms = reduce_max(e2e_ms, world, dev)
     ns_local = max(0, min(st.col_offset + st.local_cols - 1, n) - st.col_offset)
@@ -721,7 +732,9 @@ def main():
                        "exchange": exchange if world > 1 else None, "exchange_fallback": fallback,
                        "l2": ("tableau %.2f GB > L2 %d MB: inputs larger than L2" % (tableau_bytes / 1e9, l2 >> 20))
                        if flush is None else "L2 flushed (write 2xL2) before every timed step",
-                       "step": "reset (build Table I from device-resident A,b,c) + solve + extract"},
+                       "step": ("simplex_solve_lp: reset (build Table I from device-resident A,b,c) + solve + extract "
+                                "in one call (one launch, one synchronisation)") if small else
+                               "reset (build Table I from device-resident A,b,c) + solve + extract"},
             "roofline": small_roof if small else {"bound": "hbm",
                          "kernel": (f"k_update_s (rank-{look} look-ahead pass: {look} pivots per tableau "
                                     "stream, TMA loads + TMA bulk stores; runs concurrently with the "
@@ -767,7 +780,8 @@ def main():
             "small_path": small,
             "e2e": {"value": piv_e2e / (e2e_ms / 1e3), "unit": "pivots/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms": e2e_ms,
-                    "path": "simplex_reset(pinned host A,b,c) + simplex_solve + simplex_get_solution(host x,y)"},
+                    "path": "simplex_solve_lp(pinned host A,b,c -> host x,y)" if small else
+                            "simplex_reset(pinned host A,b,c) + simplex_solve + simplex_get_solution(host x,y)"},
             "gpu_launches": int(s1.kernel_launches - s0.kernel_launches),
             "clocks": clk, "parity": parity, "largest": largest, "context": PAPER_CONTEXT,
         }

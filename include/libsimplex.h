@@ -209,6 +209,18 @@ simplex_err simplex_solve(simplex_t* h, simplex_status* st);
 simplex_err simplex_get_solution(simplex_t* h, double* x, double* y, double* objective,
                                  int64_t* pivots, simplex_status* st);
 
+/* One whole LP of the handle's shape in one call: exactly simplex_reset(h, A, b, c), then
+ * simplex_solve(h), then simplex_get_solution(h, x, y, objective, pivots, st) — the same
+ * arguments (A, b, c, x, y: host or device memory, caller-owned), results, trace and errors.
+ * On the latency path (stats.path = 1: a tableau that fits one CTA's shared memory) it is ONE
+ * kernel launch that builds Table I from A, b, c, runs Steps 1-3 to termination
+ * and extracts x, y and the objective, with ONE host
+ * synchronisation instead of three: on small LPs the fixed costs around the pivots dominate
+ * (PAPER.md:161, 290).  Otherwise the three calls run in turn.  Errors: those of the three calls
+ * (ARG, NONFINITE, STATE, CUDA, NCCL); a rejected input leaves the handle as a rejected reset. */
+simplex_err simplex_solve_lp(simplex_t* h, const double* A, const double* b, const double* c, double* x,
+                             double* y, double* objective, int64_t* pivots, simplex_status* st);
+
 /* The pivot trace (SPEC.md:195-198 PivotRecord; reading c19): copy up to cap (k, r) records —
  * k the 0-based entering column, r the 1-based leaving row, in pivot order — into the caller's
  * int32 buffers k[], r[] (host or device, cap entries each); *len = records copied.  Recorded only

@@ -33,7 +33,7 @@ STATUS_NAME = {RUNNING: "RUNNING", OPTIMAL: "OPTIMAL", UNBOUNDED: "UNBOUNDED",
 
 # every symbol declared in include/libsimplex.h
 EXPORTS = ["simplex_default_options", "simplex_create", "simplex_reset", "simplex_iterate",
-           "simplex_solve", "simplex_get_solution", "simplex_get_trace", "simplex_get_tableau",
+           "simplex_solve", "simplex_solve_lp", "simplex_get_solution", "simplex_get_trace", "simplex_get_tableau",
            "simplex_tableau_hash", "simplex_get_stats", "simplex_destroy", "simplex_last_error",
            "simplex_nccl_unique_id", "simplex_partition", "simplex_version"]
 
@@ -83,6 +83,7 @@ def lib():
         L.simplex_reset.argtypes = [vp, vp, vp, vp]
         L.simplex_iterate.argtypes = [vp, i64, pi64, pint]
         L.simplex_solve.argtypes = [vp, pint]
+        L.simplex_solve_lp.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(C.c_double), pi64, pint]
         L.simplex_get_solution.argtypes = [vp, vp, vp, C.POINTER(C.c_double), pi64, pint]
         L.simplex_get_trace.argtypes = [vp, vp, vp, i64, pi64]
         L.simplex_get_tableau.argtypes = [vp, vp, i64]
@@ -279,6 +280,22 @@ class Simplex:
         st = C.c_int()
         _check(lib().simplex_solve(self._h, C.byref(st)))
         return st.value
+
+    def solve_lp(self, A, b, c, x=None, y=None):
+        """reset(A, b, c) + solve() + solution(x, y) in ONE library call (simplex_solve_lp: one
+        launch and one synchronisation on the small-tableau path).  Returns (x, y, objective,
+        pivots, status) like solution()."""
+        m, n = self.m, self.n
+        if _shape(A) != (m, n) or _shape(b) != (m,) or _shape(c) != (n,):
+            raise ValueError(f"solve_lp needs A ({m}, {n}), b ({m},), c ({n},)")
+        xo = np.empty(n) if x is None else x
+        yo = np.empty(m) if y is None else y
+        keep = []
+        obj, piv, st = C.c_double(), C.c_int64(), C.c_int()
+        _check(lib().simplex_solve_lp(self._h, _ptr(A, keep, m * n, self.device), _ptr(b, keep, m, self.device),
+                                      _ptr(c, keep, n, self.device), _out_ptr(xo, keep, n, self.device),
+                                      _out_ptr(yo, keep, m, self.device), C.byref(obj), C.byref(piv), C.byref(st)))
+        return xo, yo, obj.value, piv.value, st.value
 
     def iterate(self, max_pivots: int):
         done, st = C.c_int64(), C.c_int()

@@ -137,6 +137,18 @@ struct SlabView {
 constexpr int kProbeSlots = 64;
 constexpr int kProbeEv = 2 + 10 * kMaxLook;
 
+// k_solve_small's LP mode (simplex_solve_lp): inputs (device pointers, A row-major m x n) and
+// outputs (device: x [n], y [m], res = {objective, status, pivots, error bits}); A == NULL: off.
+struct SmallLP {
+  const double* A;
+  const double* b;
+  const double* c;
+  long long n;
+  double* x;
+  double* y;
+  double* res;
+};
+
 // Where k_select takes the entering column from.
 struct XView {
   int nparts;          // parts (ranks x virtual slabs) the columns are split over

@@ -120,6 +120,9 @@ struct simplex_s {
   double* d_y = nullptr;
   double* d_obj = nullptr;
   double* d_b = nullptr;
+  double* d_res = nullptr;              // simplex_solve_lp: {objective, status, pivots, error bits}
+  double* h_res = nullptr;              // pinned copy of it
+  double* d_stage = nullptr;            // simplex_solve_lp with host inputs: A, b, c staged on the device
   unsigned long long* d_hash = nullptr;
   double* d_fcol = nullptr;             // Phase I drive-out: staged [flag, pivot column] per rank
   long long* d_fj = nullptr;            // ... each part's first eligible column, then the minimum
@@ -217,6 +220,8 @@ struct simplex_s {
   simplex_err enqueue_pivot(int slot, int t);
   simplex_err run(long long max_pivots, long long* done);
   simplex_err run_small(long long max_pivots, long long* done);
+  simplex_err solve_lp_small(const double* A, const double* b, const double* c, double* x, double* y,
+                             double* objective, long long* pivots);
   simplex_err run_hybrid(long long max_pivots, long long* done);
   simplex_err load_lane(const double* A, const double* b, const double* c);
   simplex_err enqueue_gpu_candidate();
@@ -491,6 +496,9 @@ simplex_err simplex_s::setup(long long m_, long long n_, const double* b, const 
   RET(dalloc(&d_y, m));
   RET(dalloc(&d_obj, 1));
   RET(dalloc(&d_b, m));
+  RET(dalloc(&d_res, 4));
+  if (small) RET(dalloc(&d_stage, (size_t)(m * n + m + n)));   // simplex_solve_lp's host-input staging
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&h_res), sizeof(double) * 4, cudaHostAllocDefault));
   RET(dalloc(&d_hash, 1));
 
   // ---- exchange buffers
@@ -968,6 +976,58 @@ simplex_err simplex_s::run_small(long long max_pivots, long long* done) {
   return SIMPLEX_OK;
 }
 
+// simplex_solve_lp on the latency path: ONE launch builds Table I from A, b, c, solves and extracts
+// (k_solve_small's LP mode), ONE host synchronisation — reset + solve + get_solution of a small LP
+// without the three calls' separate round trips (small LPs are overhead-bound).
+static bool on_device(const void* p, int dev) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) && a.device == dev;
+}
+
+simplex_err simplex_s::solve_lp_small(const double* A, const double* b, const double* c, double* x, double* y,
+                                      double* objective, long long* pivots) {
+  RET(enter());
+  const double* dA = A;
+  const double* db = b;
+  const double* dc = c;
+  const bool ha = !on_device(A, device), hb = !on_device(b, device), hc = !on_device(c, device);
+  if (ha || hb || hc) {
+    if (!d_stage) RET(dalloc(&d_stage, (size_t)(m * n + m + n)));
+    if (ha) CK(cudaMemcpyAsync(d_stage, A, sizeof(double) * m * n, cudaMemcpyDefault, stream));
+    if (hb) CK(cudaMemcpyAsync(d_stage + m * n, b, sizeof(double) * m, cudaMemcpyDefault, stream));
+    if (hc) CK(cudaMemcpyAsync(d_stage + m * n + m, c, sizeof(double) * n, cudaMemcpyDefault, stream));
+    if (ha) dA = d_stage;
+    if (hb) db = d_stage + m * n;
+    if (hc) dc = d_stage + m * n + m;
+  }
+  const sx::SmallLP io{dA, db, dc, n, d_x, d_y, d_res};
+  CK(sx::launch_solve_small(slabs[0].v, LLONG_MAX, opt.tol_opt, opt.tol_piv, stream, io));
+  ++kernel_launches;
+  if (x) CK(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDefault, stream));
+  if (y) CK(cudaMemcpyAsync(y, d_y, sizeof(double) * m, cudaMemcpyDefault, stream));
+  CK(cudaMemcpyAsync(h_res, d_res, sizeof(double) * 4, cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  slot_ready = false;
+  phase = 2;
+  drive_pending = false;
+  drive_done = 0;
+  drive_rows.clear();
+  const unsigned int err = (unsigned int)h_res[3];
+  status = SIMPLEX_RUNNING;
+  it = 0;
+  if (err & sx::kErrNonFinite) return fail(SIMPLEX_E_NONFINITE, "A, b or c contains NaN or Inf");
+  if (err & sx::kErrNegRhs) return fail(SIMPLEX_E_ARG, "reset: the number of negative b entries differs from create's");
+  status = (int)h_res[1];
+  it = (long long)h_res[2];
+  if (objective) *objective = h_res[0];
+  if (pivots) *pivots = it;
+  return SIMPLEX_OK;
+}
+
 // ---- hybrid CPU lane (options.host_share, §IV)
 // The host lane's columns (host memory) from the caller's A / b / c (host or device pointers).
 simplex_err simplex_s::load_lane(const double* A, const double* b, const double* c) {
@@ -1182,6 +1242,7 @@ void simplex_s::release() {
   allocs.clear();
   if (h_state) cudaFreeHost(h_state);
   if (h_err) cudaFreeHost(h_err);
+  if (h_res) cudaFreeHost(h_res);
   if (h_slot) cudaFreeHost(h_slot);
   if (h_wcol) cudaFreeHost(h_wcol);
   if (ev_slot) cudaEventDestroy(ev_slot);
@@ -1316,6 +1377,26 @@ simplex_err simplex_get_solution(simplex_t* h, double* x, double* y, double* obj
   if (pivots) *pivots = h->it;
   if (st) *st = static_cast<simplex_status>(h->status);
   return SIMPLEX_OK;
+}
+
+simplex_err simplex_solve_lp(simplex_t* h, const double* A, const double* b, const double* c, double* x, double* y,
+                             double* objective, int64_t* pivots, simplex_status* st) {
+  g_err.clear();
+  HANDLE_OK(h);
+  if (!A || !b || !c) return fail(SIMPLEX_E_ARG, "NULL input pointer");
+  if (!h->small) {                          // the three calls, in order (same results and errors)
+    simplex_err e = simplex_reset(h, A, b, c);
+    if (e == SIMPLEX_OK) e = simplex_solve(h, nullptr);
+    if (e == SIMPLEX_OK) e = simplex_get_solution(h, x, y, objective, pivots, st);
+    return e;
+  }
+  DeviceGuard dg(h->device);
+  long long piv = 0;
+  simplex_err e = h->solve_lp_small(A, b, c, x, y, objective, &piv);
+  if (e == SIMPLEX_E_CUDA) h->faulted = true;
+  if (pivots) *pivots = piv;
+  if (st) *st = static_cast<simplex_status>(h->status);
+  return e;
 }
 
 simplex_err simplex_get_trace(simplex_t* h, int32_t* k, int32_t* r, int64_t cap, int64_t* len) {

@@ -2060,7 +2060,8 @@ __global__ void __launch_bounds__(kThreads + 64, 1) k_update_s(SlabView s, const
 // Requires one column part and no artificial columns (the engine checks).
 constexpr int kSmallMaxQ = 8;                        // tableau width <= 256 columns
 template <int NT, int NQ>
-__global__ void __launch_bounds__(NT, 1) k_solve_small(SlabView s, long long stop_at, double tol_opt, double tol_piv) {
+__global__ void __launch_bounds__(NT, 1) k_solve_small(SlabView s, long long stop_at, double tol_opt, double tol_piv,
+                                                       SmallLP io) {
   constexpr int NW = NT / 32;                        // NQ: columns per lane (cols <= 32 * NQ)
   extern __shared__ __align__(16) double smem[];
   const int rows = s.rows, m = rows - 1;
@@ -2074,17 +2075,65 @@ __global__ void __launch_bounds__(NT, 1) k_solve_small(SlabView s, long long sto
   __shared__ Cand sh_k;                              // Step-1 result for the next pivot
   DevState* st = s.st;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int pend = st->pend_r;                       // a deferred pivot row of another path
-  for (int i = wid; i < rows; i += NW) {
-    const double* src = (i == pend) ? s.rownorm : s.T + (long long)i * s.ld;
-    for (int j = lane; j < cols; j += 32) T[(size_t)i * cols + j] = src[j];
+  long long it;
+  int status;
+  if (io.A) {
+    // LP mode (simplex_solve_lp): Table I is built right here from the caller's
+    // A, b, c — the slack basis, row 0 = -c, rows i = [a_i, e_i, b_i] (k_build's values; c10: no
+    // Z column) — with k_build's validation (finite inputs, b >= 0: a small handle has no Phase I)
+    const long long n = io.n;
+    __shared__ unsigned int sh_err;
+    if (tid == 0) sh_err = 0u;
+    __syncthreads();
+    unsigned int err = 0u;
+    for (int i = wid; i < rows; i += NW)
+      for (int j = lane; j < cols; j += 32) {
+        double v;
+        if (j == rhs) {
+          v = i == 0 ? 0.0 : io.b[i - 1];
+          if (i > 0 && !isfinite(v)) err |= kErrNonFinite;
+          if (i > 0 && v < 0.0) err |= kErrNegRhs;
+        } else if (j < n) {
+          v = i == 0 ? io.c[j] : io.A[(long long)(i - 1) * n + j];
+          if (!isfinite(v)) err |= kErrNonFinite;
+          if (i == 0) v = -v;
+        } else {
+          v = (i >= 1 && j - n == i - 1) ? 1.0 : 0.0;
+        }
+        T[(size_t)i * cols + j] = v;
+      }
+    for (int i = tid; i < m; i += NT) basis[i] = (int)(n + i);
+    if (err) atomicOr(&sh_err, err);
+    it = 0;
+    status = kRunning;
+    __syncthreads();
+    if (sh_err) {                                      // invalid input: the built tableau, no pivots
+      status = kFault;
+      if (tid == 0) st->err = sh_err;
+    }
+    if (tid == 0) {
+      st->it = 0;
+      st->stop_at = LLONG_MAX;
+      st->status = kRunning;
+      st->phase = 2;
+      st->pw = s.w;
+      st->drive_next = 0;
+      st->sb[0] = st->sb[1] = 0;
+      if (!sh_err) st->err = 0u;
+    }
+  } else {
+    const int pend = st->pend_r;                     // a deferred pivot row of another path
+    for (int i = wid; i < rows; i += NW) {
+      const double* src = (i == pend) ? s.rownorm : s.T + (long long)i * s.ld;
+      for (int j = lane; j < cols; j += 32) T[(size_t)i * cols + j] = src[j];
+    }
+    for (int i = tid; i < m; i += NT) basis[i] = s.basis[i];
+    it = st->it;
+    status = st->status;
   }
-  for (int i = tid; i < m; i += NT) basis[i] = s.basis[i];
   const long long cap = st->cap;
-  const int pw = st->pw;
+  const int pw = io.A ? s.w : st->pw;
   const int rule = s.rule;
-  long long it = st->it;
-  int status = st->status;
   __syncthreads();
   if (wid == 0) {                                    // Step 1 on the starting row 0
     Cand c = cand_none();
@@ -2181,9 +2230,28 @@ __global__ void __launch_bounds__(NT, 1) k_solve_small(SlabView s, long long sto
   for (int i = tid; i < m; i += NT) s.basis[i] = basis[i];
   if (tid == 0) {
     st->it = it;
-    st->status = status;
+    st->status = status == kFault ? kRunning : status;
     st->pend_r = -1;
     st->go = 0;
+  }
+  if (io.A) {
+    // LP mode: the solution too (k_extract's definition): x_j = rhs of the row
+    // where x_j is basic (0 if non-basic), y_i = T[0][n+i], objective = T[0][rhs]
+    const long long n = io.n;
+    if (io.x) {
+      for (long long j = tid; j < n; j += NT) io.x[j] = 0.0;
+      __syncthreads();
+      for (int i = tid; i < m; i += NT)
+        if (basis[i] < n) io.x[basis[i]] = T[(size_t)(i + 1) * cols + rhs];
+    }
+    if (io.y)
+      for (int i = tid; i < m; i += NT) io.y[i] = T[n + i];
+    if (tid == 0) {
+      io.res[0] = T[rhs];
+      io.res[1] = (double)(status == kFault ? kRunning : status);
+      io.res[2] = (double)it;
+      io.res[3] = (double)st->err;
+    }
   }
 }
 
@@ -2204,7 +2272,7 @@ size_t small_smem_max() {
 
 template <int NT, int NQ>
 static cudaError_t launch_small_nt(const SlabView& s, long long stop_at, double tol_opt, double tol_piv,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, const SmallLP& io) {
   static size_t set = 0;                             // opt-in size already granted (per instantiation)
   const size_t smem = small_smem_bytes(s.rows, s.w);
   if (smem > set) {
@@ -2213,28 +2281,34 @@ static cudaError_t launch_small_nt(const SlabView& s, long long stop_at, double 
     if (e != cudaSuccess) return e;
     set = small_smem_max();
   }
-  k_solve_small<NT, NQ><<<1, NT, smem, st>>>(s, stop_at, tol_opt, tol_piv);
+  k_solve_small<NT, NQ><<<1, NT, smem, st>>>(s, stop_at, tol_opt, tol_piv, io);
   return cudaGetLastError();
 }
 
 template <int NQ>
 static cudaError_t launch_small_q(int nt, const SlabView& s, long long stop_at, double tol_opt, double tol_piv,
-                                  cudaStream_t st) {
-  if (nt >= 1024) return launch_small_nt<1024, NQ>(s, stop_at, tol_opt, tol_piv, st);
-  if (nt >= 512) return launch_small_nt<512, NQ>(s, stop_at, tol_opt, tol_piv, st);
-  if (nt >= 256) return launch_small_nt<256, NQ>(s, stop_at, tol_opt, tol_piv, st);
-  return launch_small_nt<128, NQ>(s, stop_at, tol_opt, tol_piv, st);
+                                  cudaStream_t st, const SmallLP& io) {
+  if (nt >= 1024) return launch_small_nt<1024, NQ>(s, stop_at, tol_opt, tol_piv, st, io);
+  if (nt >= 512) return launch_small_nt<512, NQ>(s, stop_at, tol_opt, tol_piv, st, io);
+  return launch_small_nt<256, NQ>(s, stop_at, tol_opt, tol_piv, st, io);
 }
 
 // 512 threads per CTA (measured, scripts/small_probe.py: 64x64 3.5 us/pivot vs 4.4 at 256 and
 // 6.4 at 128; 1024 no faster); 4 or 8 columns per lane
 cudaError_t launch_solve_small(const SlabView& s, long long stop_at, double tol_opt, double tol_piv,
-                               cudaStream_t st) {
+                               cudaStream_t st, const SmallLP& io) {
   int nt = 512;
   if (const char* e = experiment_env("SIMPLEX_SMALL_THREADS")) nt = std::atoi(e);
   if (s.w + 1 > 32 * kSmallMaxQ) return cudaErrorInvalidValue;
-  if (s.w + 1 <= 128) return launch_small_q<4>(nt, s, stop_at, tol_opt, tol_piv, st);
-  return launch_small_q<kSmallMaxQ>(nt, s, stop_at, tol_opt, tol_piv, st);
+  // columns per lane: the smallest instantiated NQ >= cols / 32 (64^2: 129 columns -> 5, so no lane
+  // carries predicated-off columns through the update)
+  const int q = (s.w + 1 + 31) / 32;
+  if (q <= 2) return launch_small_q<2>(nt, s, stop_at, tol_opt, tol_piv, st, io);
+  if (q <= 3) return launch_small_q<3>(nt, s, stop_at, tol_opt, tol_piv, st, io);
+  if (q <= 4) return launch_small_q<4>(nt, s, stop_at, tol_opt, tol_piv, st, io);
+  if (q <= 5) return launch_small_q<5>(nt, s, stop_at, tol_opt, tol_piv, st, io);
+  if (q <= 6) return launch_small_q<6>(nt, s, stop_at, tol_opt, tol_piv, st, io);
+  return launch_small_q<kSmallMaxQ>(nt, s, stop_at, tol_opt, tol_piv, st, io);
 }
 
 // ------------------------------------------------------------------ flush / extract / hash

@@ -68,8 +68,10 @@ cudaError_t launch_update_s(int cfg, const SlabView& s, int S, const double* src
 // k_solve_small: the whole solve of a tableau that fits in one CTA's shared memory, one launch
 size_t small_smem_bytes(int rows, int w);
 size_t small_smem_max();
+// io.A != NULL (simplex_solve_lp): build Table I from device A, b, c in the kernel and write
+// x, y and res = {objective, status, pivots, error bits} after the solve
 cudaError_t launch_solve_small(const SlabView& s, long long stop_at, double tol_opt, double tol_piv,
-                               cudaStream_t st);
+                               cudaStream_t st, const SmallLP& io = SmallLP{});
 cudaError_t launch_phase1_row0(const SlabView& s, cudaStream_t st);
 cudaError_t launch_phase2_row0(const SlabView& s, long long n, cudaStream_t st);
 // Phase I drive-out on the device (reading p4; kernels.cu k_drive_*)

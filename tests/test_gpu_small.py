@@ -26,9 +26,12 @@ def sx(cuda_device):
     return sx
 
 
+DEVICE_LOOP = (0, 3)    # graph-segment device loop (3: with the shared-memory selection k_look2)
+
+
 def small_solve(sx, A, b, c, expect_path=1, **kw):
     with sx.Simplex(A, b, c, **kw) as s:
-        assert s.stats().path == expect_path
+        assert s.stats().path in (expect_path if isinstance(expect_path, tuple) else (expect_path,))
         st = s.solve()
         x, y, obj, piv, st2 = s.solution()
         k, r = s.trace()
@@ -127,7 +130,7 @@ def test_largest_fitting_and_first_not_fitting(sx):
     A, b, c = lpgen.dense_lp(100, 150, 4)
     assert_same(small_solve(sx, A, b, c), oracle.solve(A, b, c, keep_tableau=True))
     A, b, c = lpgen.dense_lp(120, 150, 4)
-    assert_same(small_solve(sx, A, b, c, expect_path=0), oracle.solve(A, b, c, keep_tableau=True))
+    assert_same(small_solve(sx, A, b, c, expect_path=3), oracle.solve(A, b, c, keep_tableau=True))
 
 
 def test_explicit_lookahead_keeps_device_loop(sx):
@@ -135,8 +138,8 @@ def test_explicit_lookahead_keeps_device_loop(sx):
     other kernels stay testable at small sizes."""
     A, b, c = lpgen.dense_lp(64, 64, 5)
     o = oracle.solve(A, b, c, keep_tableau=True)
-    for look in (1, 16):
-        assert_same(small_solve(sx, A, b, c, expect_path=0, lookahead=look), o)
+    for look, path in ((1, 0), (16, 3)):
+        assert_same(small_solve(sx, A, b, c, expect_path=path, lookahead=look), o)
 
 
 def test_phase1_and_virtual_ranks_use_device_loop(sx):
@@ -144,6 +147,73 @@ def test_phase1_and_virtual_ranks_use_device_loop(sx):
     b2 = b.copy()
     b2[3] = -1.0
     with sx.Simplex(A, b2, c) as s:
-        assert s.stats().path == 0
+        assert s.stats().path == 3                        # device loop (one part: k_look2)
     with sx.Simplex(A, b, c, virtual_ranks=2) as s:
-        assert s.stats().path == 0
+        assert s.stats().path == 0                        # several parts: k_mblock / k_mlook
+
+
+# simplex_solve_lp: reset + solve + get_solution in ONE library call; on the small path ONE launch
+# (Table I built in the kernel from A, b, c; the solution extracted in it) and one synchronisation.
+# Bar: the three calls' results bit for bit == the oracle's, on one handle reused across LPs.
+def lp_solve(s, A, b, c, **kw):
+    x, y, obj, piv, st = s.solve_lp(A, b, c, **kw)
+    k, r = s.trace()
+    T, _ = s.tableau()
+    return dict(status=st, x=np.asarray(x.cpu() if hasattr(x, "cpu") else x), y=np.asarray(y.cpu() if hasattr(y, "cpu") else y),
+                obj=obj, pivots=piv, k=k, r=r, T=T, hash=s.tableau_hash())
+
+
+def test_solve_lp_seeds_one_handle(sx):
+    A0, b0, c0 = lpgen.dense_lp(64, 64, 1000)
+    with sx.Simplex(A0, b0, c0) as s:
+        assert s.stats().path == 1
+        for seed in range(1, 41):
+            A, b, c = lpgen.dense_lp(64, 64, seed)
+            assert_same(lp_solve(s, A, b, c), oracle.solve(A, b, c, keep_tableau=True))
+
+
+def test_solve_lp_device_buffers(sx):
+    import torch
+    A, b, c = lpgen.dense_lp(64, 64, 7)
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    Ad, bd, cd = (torch.from_numpy(v).cuda() for v in (A, b, c))
+    xd, yd = torch.empty(64, dtype=torch.float64, device="cuda"), torch.empty(64, dtype=torch.float64, device="cuda")
+    with sx.Simplex(Ad, bd, cd) as s:
+        assert_same(lp_solve(s, Ad, bd, cd, x=xd, y=yd), o)
+        assert_same(lp_solve(s, A, b, cd, x=xd), o)          # mixed host / device inputs
+
+
+@pytest.mark.parametrize("name", ["classic", "chvatal", "unbounded", "beale", "entering_tie", "ratio_tie",
+                                  "zero_iteration"])
+def test_solve_lp_worked_examples(sx, name):
+    A, b, c = {"classic": F.classic, "chvatal": F.chvatal, "unbounded": F.unbounded_1d, "beale": F.beale}.get(
+        name, lambda: tuple(np.array(GOLD[name][k], float) for k in ("A", "b", "c")))()
+    with sx.Simplex(A, b, c) as s:
+        assert s.stats().path == 1
+        assert_same(lp_solve(s, A, b, c), oracle.solve(A, b, c, keep_tableau=True))
+
+
+def test_solve_lp_rejects_then_recovers(sx):
+    A, b, c = lpgen.dense_lp(40, 30, 3)
+    with sx.Simplex(A, b, c) as s:
+        bad = A.copy()
+        bad[5, 7] = np.nan
+        with pytest.raises(sx.SimplexError) as e:
+            s.solve_lp(bad, b, c)
+        assert e.value.code == sx.E_NONFINITE
+        nb = b.copy()
+        nb[3] = -1.0
+        with pytest.raises(sx.SimplexError) as e:
+            s.solve_lp(A, nb, c)
+        assert e.value.code == sx.E_ARG
+        assert_same(lp_solve(s, A, b, c), oracle.solve(A, b, c, keep_tableau=True))
+        s.reset(A, b, c)                                  # the three calls still agree afterwards
+        assert s.solve() == sx.OPTIMAL
+
+
+def test_solve_lp_large_path_is_the_three_calls(sx):
+    A, b, c = lpgen.dense_lp(300, 400, 5)                 # 701 columns: not the one-CTA path
+    o = oracle.solve(A, b, c, keep_tableau=True)
+    with sx.Simplex(A, b, c) as s:
+        assert s.stats().path != 1
+        assert_same(lp_solve(s, A, b, c), o)
