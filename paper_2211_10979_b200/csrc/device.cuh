@@ -122,7 +122,6 @@ struct SlabView {
   double2* hand;
   int look_nt;         // threads per CTA of k_look2 (0: k_lookahead)
   int look_qc, look_qr;     // k_look2 instantiation: own column / row slots per thread
-  int look_os;              // 1: its own-bank operands in shared memory, 0: in the hand-off slots
   int look_nqc, look_nqr;   // own columns / rows per thread actually used (hand-off layout)
   unsigned long long* probe;   // experiment hook (SIMPLEX_PROBE): selection phase timestamps, else NULL
   int time_pass;       // 1: k_update_s times itself on the device (DevState pass_*) — the way to

@@ -1077,13 +1077,11 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
 // the selection issue- and dependency-bound: each phase re-read up to 31 chain operands per
 // element through L2 (the cluster barrier's acquire invalidates L1), every thread re-loaded up to
 // 33 broadcast scalars, and the chains carried a bit-test + two selects per operand.  Here:
-//   * the previous bank's chain operands of a thread's elements (PS) live in SHARED memory as
-//     double2 pairs [q][u/2][tid] (one conflict-free LDS.128 per two operands), copied in at
-//     launch start from the global hand-off s.hand[bpre], which the previous launch wrote from the
-//     SAME thread positions; the own bank (this launch's pivots: col_u[i] of its rows, prow_u[j]
-//     of its columns) lives in shared memory too when it fits (OS), else in the hand-off slots
-//     s.hand[bown] themselves (own writes read back through L2, every load of a phase in flight
-//     at once);
+//   * every chain operand of a thread's elements lives in SHARED memory as double2 pairs
+//     [q][u/2][tid] (one conflict-free LDS.128 per two operands): the own bank (this launch's
+//     pivots: col_u[i] of its rows, prow_u[j] of its columns) and (PS) the previous bank, copied
+//     in at launch start from the global hand-off s.hand[bpre], which the previous launch wrote
+//     from the SAME thread positions (without PS: read from the hand-off);
 //   * the running objective row R0 and rhs column RHS of own elements stay in shared memory;
 //   * a phase's broadcast operands (prow_u[k] of both banks + the previous pivot's rhs entry;
 //     col_u[r] of both banks + col_t[0]) are loaded ONCE per warp, one lane per value, behind the
@@ -1095,7 +1093,7 @@ __global__ void __launch_bounds__(kLookThreads) k_lookahead(SlabView s, const do
 //   * chunks of 32 consecutive elements are dealt to the cluster's CTAs round-robin, so small
 //     tableaux keep every SM of the cluster busy.
 // The pass (k_update_s) still gets colS / prowS from global memory.
-template <int NT, bool PS, bool OS, int QC, int QR>
+template <int NT, bool PS, int QC, int QR>
 __global__ void __launch_bounds__(NT, 1) k_look2(SlabView s, const double* __restrict__ T, int S, int bown,
                                                  int bpre, int nqc, int nqr, double tol_opt, double tol_piv) {
   pdl_launch_dependents();                            // the previous block's pass may start now
@@ -1117,9 +1115,9 @@ __global__ void __launch_bounds__(NT, 1) k_look2(SlabView s, const double* __res
   const int pw = st->pw;
   const int mwords = ((rows + 31) / 32 + 3) & ~3;
   unsigned int* piv_mark = sm2;
-  double2* OP = reinterpret_cast<double2*>(sm2 + mwords);          // OS: [QC][H][NT] own prow_u[j]
-  double2* OC = OP + (OS ? (size_t)QC * H * NT : 0);                // OS: [QR][H][NT] own col_u[i]
-  double* R0s = reinterpret_cast<double*>(OC + (OS ? (size_t)QR * H * NT : 0));   // [QC][NT]
+  double2* OP = reinterpret_cast<double2*>(sm2 + mwords);          // [QC][H][NT] own prow_u[j]
+  double2* OC = OP + (size_t)QC * H * NT;                           // [QR][H][NT] own col_u[i]
+  double* R0s = reinterpret_cast<double*>(OC + (size_t)QR * H * NT);   // [QC][NT]
   double* RHSs = R0s + (size_t)QC * NT;                                          // [QR][NT]
   double2* PPs = reinterpret_cast<double2*>(RHSs + (size_t)QR * NT);    // PS: [QC][H][NT]
   double2* PCs = PPs + (size_t)QC * H * NT;                              // PS: [QR][H][NT]
@@ -1160,7 +1158,7 @@ __global__ void __launch_bounds__(NT, 1) k_look2(SlabView s, const double* __res
   } while (0)
   SX_PROBE(0);
   // chain operand pair v of own column / row q: previous bank (smem copy, or the hand-off, read
-  // only for valid elements) and own bank (smem, or this launch's hand-off slots)
+  // only for valid elements) and own bank (smem)
   auto pre_c = [&](int q, int v) -> double2 {
     if (PS) return PPs[((size_t)q * H + v) * NT + tid];
     return jq[q] < ld ? __ldg(hpre + ((size_t)q * H + v) * G + gtid) : make_double2(0.0, 0.0);
@@ -1169,21 +1167,13 @@ __global__ void __launch_bounds__(NT, 1) k_look2(SlabView s, const double* __res
     if (PS) return PCs[((size_t)q * H + v) * NT + tid];
     return iq[q] < rows ? __ldg(hpre + ((size_t)(nqc + q) * H + v) * G + gtid) : make_double2(0.0, 0.0);
   };
-  auto own_c = [&](int q, int v) -> double2 {
-    if (OS) return OP[((size_t)q * H + v) * NT + tid];
-    return jq[q] < ld ? __ldcg(hown + ((size_t)q * H + v) * G + gtid) : make_double2(0.0, 0.0);
-  };
-  auto own_r = [&](int q, int v) -> double2 {
-    if (OS) return OC[((size_t)q * H + v) * NT + tid];
-    return iq[q] < rows ? __ldcg(hown + ((size_t)(nqc + q) * H + v) * G + gtid) : make_double2(0.0, 0.0);
-  };
+  auto own_c = [&](int q, int v) -> double2 { return OP[((size_t)q * H + v) * NT + tid]; };
+  auto own_r = [&](int q, int v) -> double2 { return OC[((size_t)q * H + v) * NT + tid]; };
   auto own_c_set = [&](int q, int u, double val) {
-    if (OS) reinterpret_cast<double*>(OP + ((size_t)q * H + (u >> 1)) * NT + tid)[u & 1] = val;
-    else reinterpret_cast<double*>(hown + ((size_t)q * H + (u >> 1)) * G + gtid)[u & 1] = val;
+    reinterpret_cast<double*>(OP + ((size_t)q * H + (u >> 1)) * NT + tid)[u & 1] = val;
   };
   auto own_r_set = [&](int q, int u, double val) {
-    if (OS) reinterpret_cast<double*>(OC + ((size_t)q * H + (u >> 1)) * NT + tid)[u & 1] = val;
-    else reinterpret_cast<double*>(hown + ((size_t)(nqc + q) * H + (u >> 1)) * G + gtid)[u & 1] = val;
+    reinterpret_cast<double*>(OC + ((size_t)q * H + (u >> 1)) * NT + tid)[u & 1] = val;
   };
   const int vpre = (spre + 1) >> 1;                   // pairs holding the spre previous operands
   if (PS && spre > 0) {
@@ -1249,7 +1239,7 @@ __global__ void __launch_bounds__(NT, 1) k_look2(SlabView s, const double* __res
       __syncwarp();
     }
     SX_PROBE(2 + 10 * t);
-    // own-bank operands of the own rows, every load in flight at once (OS: shared memory)
+    // own-bank operands of the own rows
     double2 ob[QR][H];
 #pragma unroll
     for (int v = 0; v < H; ++v)
@@ -1468,23 +1458,21 @@ __global__ void __launch_bounds__(NT, 1) k_look2(SlabView s, const double* __res
   }
 #undef SX_PROBE
 #undef SX_TIMER
-  // hand-off: own R0 / RHS back to global; OS: the own bank's operands to s.hand[bown] (the next
-  // launch's previous bank, read by the same thread positions; without OS they are already there)
+  // hand-off: own R0 / RHS back to global, the own bank's operands to s.hand[bown] (the next
+  // launch's previous bank, read by the same thread positions)
   const int vown = (t + 1) >> 1;
 #pragma unroll
   for (int q = 0; q < QC; ++q) {
     if (jq[q] < ld) {
       s.R0[jq[q]] = R0s[q * NT + tid];
-      if (OS)
-        for (int v = 0; v < vown; ++v) hown[((size_t)q * H + v) * G + gtid] = OP[((size_t)q * H + v) * NT + tid];
+      for (int v = 0; v < vown; ++v) hown[((size_t)q * H + v) * G + gtid] = OP[((size_t)q * H + v) * NT + tid];
     }
   }
 #pragma unroll
   for (int q = 0; q < QR; ++q) {
     if (iq[q] < rows) {
       s.RHS[iq[q]] = RHSs[q * NT + tid];
-      if (OS)
-        for (int v = 0; v < vown; ++v)
+      for (int v = 0; v < vown; ++v)
           hown[((size_t)(nqc + q) * H + v) * G + gtid] = OC[((size_t)q * H + v) * NT + tid];
     }
   }
@@ -2510,24 +2498,24 @@ size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int*
   return mark;
 }
 
-// k_look2 instantiations: (own columns QC, own rows QR per thread, own bank in shared memory OS);
-// a slab takes the first that covers its (nqc, nqr) and fits in shared memory WITH the previous
-// bank (the pipelined launches), else k_lookahead.  Measured (round 3, pipelined blocks): 1000^2
+// k_look2 instantiations: (own columns QC, own rows QR per thread); a slab takes the first that
+// covers its (nqc, nqr) and fits in shared memory WITH the previous bank (the pipelined
+// launches), else k_lookahead.  Measured (round 3, pipelined blocks): 1000^2
 // 110-118 us (k_lookahead ~135), 2000^2 115-121 (134), 4000^2 157-166 (166); with the own bank in
-// the hand-off slots (OS = 0, the only way 8000^2 fits) 388 us against k_lookahead's 343 — so the
-// OS = 0 configurations are not offered and 8000^2 and larger keep k_lookahead.
-static const int kLook2Q[][3] = {{1, 1, 1}, {2, 1, 1}};   // (ld >= rows: QR <= QC always)
+// the hand-off slots (the only way 8000^2 fits; built, measured, removed) 388 us against
+// k_lookahead's 343 — so 8000^2 and larger keep k_lookahead.
+static const int kLook2Q[][2] = {{1, 1}, {2, 1}};   // (ld >= rows: QR <= QC always)
 constexpr int kLook2NQ = sizeof(kLook2Q) / sizeof(kLook2Q[0]);
 
-size_t look2_smem(const SlabView& s, int nt, bool ps, bool os, int qc, int qr) {
+size_t look2_smem(const SlabView& s, int nt, bool ps, int qc, int qr) {
   const size_t mark = (size_t)(((s.rows + 31) / 32 + 3) & ~3) * sizeof(unsigned int);
   const size_t q = (size_t)(qc + qr), bank = q * nt * (kMaxLook / 2) * sizeof(double2);
-  return mark + q * nt * sizeof(double) + (os ? bank : 0) + (ps ? bank : 0);
+  return mark + q * nt * sizeof(double) + bank + (ps ? bank : 0);
 }
 
-template <bool PS, bool OS, int QC, int QR>
+template <bool PS, int QC, int QR>
 static cudaError_t look2_attr(int cluster, int* nclusters) {
-  auto kern = k_look2<256, PS, OS, QC, QR>;
+  auto kern = k_look2<256, PS, QC, QR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLook2SmemMax);
   if (e != cudaSuccess) return e;
@@ -2540,8 +2528,8 @@ static cudaError_t look2_attr(int cluster, int* nclusters) {
 template <bool PS>
 static cudaError_t look2_attr_q(int qi, int cluster, int* n) {
   switch (qi) {
-    case 0: return look2_attr<PS, true, 1, 1>(cluster, n);
-    default: return look2_attr<PS, true, 2, 1>(cluster, n);
+    case 0: return look2_attr<PS, 1, 1>(cluster, n);
+    default: return look2_attr<PS, 2, 1>(cluster, n);
   }
 }
 
@@ -2550,8 +2538,8 @@ long long look2_prepare(SlabView* s, int cluster) {
   const long long G = (long long)cluster * nt;
   const int nqc = (int)((s->ld + G - 1) / G), nqr = (int)((s->rows + G - 1) / G);
   for (int qi = 0; qi < kLook2NQ; ++qi) {
-    const int qc = kLook2Q[qi][0], qr = kLook2Q[qi][1], os = kLook2Q[qi][2];
-    if (qc < nqc || qr < nqr || look2_smem(*s, nt, true, os, qc, qr) > kLook2SmemMax) continue;
+    const int qc = kLook2Q[qi][0], qr = kLook2Q[qi][1];
+    if (qc < nqc || qr < nqr || look2_smem(*s, nt, true, qc, qr) > kLook2SmemMax) continue;
     int n0 = 0, n1 = 0;
     cudaError_t e = look2_attr_q<false>(qi, cluster, &n0);
     if (e == cudaSuccess) e = look2_attr_q<true>(qi, cluster, &n1);
@@ -2562,7 +2550,6 @@ long long look2_prepare(SlabView* s, int cluster) {
     s->look_nt = nt;
     s->look_qc = qc;
     s->look_qr = qr;
-    s->look_os = os;
     s->look_nqc = nqc;
     s->look_nqr = nqr;
     return 2LL * (nqc + nqr) * (kMaxLook / 2) * G;   // hand-off double2 entries (two banks)
@@ -2570,13 +2557,13 @@ long long look2_prepare(SlabView* s, int cluster) {
   return 0;
 }
 
-template <bool PS, bool OS, int QC, int QR>
+template <bool PS, int QC, int QR>
 static cudaError_t look2_launch(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
                                 double tol_piv, int cluster, cudaStream_t st) {
   cudaLaunchAttribute attr[1];
-  cudaLaunchConfig_t cfg = lookahead_config(cluster, look2_smem(s, 256, PS, OS, QC, QR), st, attr);
+  cudaLaunchConfig_t cfg = lookahead_config(cluster, look2_smem(s, 256, PS, QC, QR), st, attr);
   cfg.blockDim = dim3(256);
-  return cudaLaunchKernelEx(&cfg, k_look2<256, PS, OS, QC, QR>, s, T, S, bown, bpre, s.look_nqc, s.look_nqr,
+  return cudaLaunchKernelEx(&cfg, k_look2<256, PS, QC, QR>, s, T, S, bown, bpre, s.look_nqc, s.look_nqr,
                             tol_opt, tol_piv);
 }
 
@@ -2584,8 +2571,8 @@ template <bool PS>
 static cudaError_t look2_launch_q(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,
                                   double tol_piv, int cluster, cudaStream_t st) {
   const int qc = s.look_qc, qr = s.look_qr;
-  if (qc == 1 && qr == 1) return look2_launch<PS, true, 1, 1>(s, T, S, bown, bpre, tol_opt, tol_piv, cluster, st);
-  return look2_launch<PS, true, 2, 1>(s, T, S, bown, bpre, tol_opt, tol_piv, cluster, st);
+  if (qc == 1 && qr == 1) return look2_launch<PS, 1, 1>(s, T, S, bown, bpre, tol_opt, tol_piv, cluster, st);
+  return look2_launch<PS, 2, 1>(s, T, S, bown, bpre, tol_opt, tol_piv, cluster, st);
 }
 
 cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown, int bpre, double tol_opt,

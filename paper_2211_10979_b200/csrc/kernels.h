@@ -43,7 +43,7 @@ size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int*
 // k_look2 (the default single-part selection when its own-bank operands fit in shared memory):
 // own column / row slots per thread and the dynamic shared memory (ps: previous bank too)
 constexpr size_t kLook2SmemMax = 220 * 1024;
-size_t look2_smem(const SlabView& s, int nt, bool ps, bool os, int qc, int qr);
+size_t look2_smem(const SlabView& s, int nt, bool ps, int qc, int qr);
 // picks the k_look2 instantiation for the slab (s->look_*) and sets the kernel attributes; returns
 // the hand-off size in double2 entries, 0 if k_look2 does not fit (the slab keeps k_lookahead)
 long long look2_prepare(SlabView* s, int cluster);
