@@ -2594,8 +2594,8 @@ cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown
 // k_update_s configurations (rows per stage R, stages K); shared memory ~ K*R*(cw+16)*8 B.
 // Measured (scripts/pipe_sweep.sh): {4, 12} is the fastest pass on its own.  When the pass is
 // shorter than the concurrent look-ahead selection (4000^2) the gentle {2, 16} gives the shorter
-// pipelined block, because it slows the selection's dependent HBM reads least; when the two are
-// about as long (2 GB at 8000^2) {6, 7} does; a larger tableau makes the pass the critical path.
+// pipelined block, because it slows the selection's dependent HBM reads least; from 8000^2 on the
+// pass is the critical path (round 3, scripts/cfg8000_r03.sh) and {4, 12} the shortest block.
 // SIMPLEX_PASS_CFG overrides the choice (experiments).
 struct PassCfg { int R, K; };
 static const PassCfg kPassCfgs[] = {{4, 12}, {4, 10}, {8, 5}, {6, 7}, {2, 16}, {4, 8}};
@@ -2604,7 +2604,8 @@ int pass_cfg_choice(bool pipelined, double pass_bytes) {
   const int v = e ? std::atoi(e) : -1;
   if (v >= 0 && v < 6) return v;
   if (pipelined && pass_bytes < 1e9) return 4;     // selection-bound (4000^2: 210 us blocks, 104 us pass)
-  if (pipelined && pass_bytes < 4e9) return 3;     // balanced (8000^2: 370 us blocks vs 381 with {2, 16})
+  // round 3: with the selection at 308 us next to the 8000^2 pass, the fastest pass is the bound:
+  // {4, 12} 335.5-337.4 us blocks (pass 323.5 us, 96.3 % of HBM) vs {6, 7} 344.4 (332.5)
   return 0;
 }
 int update_s_max(int S) { return S <= 4 ? 4 : S <= 8 ? 8 : S <= kMaxLook ? kMaxLook : kColS; }
