@@ -2500,7 +2500,7 @@ size_t lookahead_smem(const SlabView& s, int cluster, bool cache, int* nqc, int*
 
 // k_look2 instantiations: (own columns QC, own rows QR per thread); a slab takes the first that
 // covers its (nqc, nqr) and fits in shared memory WITH the previous bank (the pipelined
-// launches), else k_lookahead.  Measured (round 3, pipelined blocks): 1000^2
+// launches), else k_lookahead.  Measured (round 2b, pipelined blocks): 1000^2
 // 110-118 us (k_lookahead ~135), 2000^2 115-121 (134), 4000^2 157-166 (166); with the own bank in
 // the hand-off slots (the only way 8000^2 fits; built, measured, removed) 388 us against
 // k_lookahead's 343 — so 8000^2 and larger keep k_lookahead.
@@ -2595,7 +2595,7 @@ cudaError_t launch_lookahead(const SlabView& s, const double* T, int S, int bown
 // Measured (scripts/pipe_sweep.sh): {4, 12} is the fastest pass on its own.  When the pass is
 // shorter than the concurrent look-ahead selection (4000^2) the gentle {2, 16} gives the shorter
 // pipelined block, because it slows the selection's dependent HBM reads least; from 8000^2 on the
-// pass is the critical path (round 3, scripts/cfg8000_r03.sh) and {4, 12} the shortest block.
+// pass is the critical path (round 2b, scripts/cfg8000_r02b.sh) and {4, 12} the shortest block.
 // SIMPLEX_PASS_CFG overrides the choice (experiments).
 struct PassCfg { int R, K; };
 static const PassCfg kPassCfgs[] = {{4, 12}, {4, 10}, {8, 5}, {6, 7}, {2, 16}, {4, 8}};
@@ -2604,7 +2604,7 @@ int pass_cfg_choice(bool pipelined, double pass_bytes) {
   const int v = e ? std::atoi(e) : -1;
   if (v >= 0 && v < 6) return v;
   if (pipelined && pass_bytes < 1e9) return 4;     // selection-bound (4000^2: 210 us blocks, 104 us pass)
-  // round 3: with the selection at 308 us next to the 8000^2 pass, the fastest pass is the bound:
+  // round 2b: with the selection at 308 us next to the 8000^2 pass, the fastest pass is the bound:
   // {4, 12} 335.5-337.4 us blocks (pass 323.5 us, 96.3 % of HBM) vs {6, 7} 344.4 (332.5)
   return 0;
 }

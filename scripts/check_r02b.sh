@@ -1,5 +1,5 @@
 #!/bin/bash
-# full GPU suite + smoke + bench lines (round 3)
+# full GPU suite + smoke + bench lines (round 2b)
 o=gpurun_out/check; mkdir -p $o
 python -c "import __graft_entry__ as g; g.smoke()" > $o/smoke.txt 2>&1; tail -3 $o/smoke.txt
 timeout 2400 python -m pytest -q -m gpu tests > $o/pytest.txt 2>&1; echo "pytest rc=$?" >> $o/pytest.txt; tail -4 $o/pytest.txt

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-3 measurement set (GPU box): smoke, bench lines for every single-GPU config and the reference
+# Round-2b measurement set (GPU box): smoke, bench lines for every single-GPU config and the reference
 # (oracle) arm, torchrun N=1, then the ncu launch list of the default bench command and full
 # captures (with source) of the hot kernels.  Outputs in gpurun_out/final3/.
 o=gpurun_out/final3

@@ -1,4 +1,4 @@
-// FP64 latency / throughput microbenchmark (round 3): dependent DFMA / DADD latency,
+// FP64 latency / throughput microbenchmark (round 2b): dependent DFMA / DADD latency,
 // __ddiv_rn latency and per-SM division throughput.   nvcc -gencode arch=compute_100a,code=sm_100a -O3
 // -o build/lat_probe scripts/fp64_latency.cu   (measured on B200: DFMA 8.1 cycles, __ddiv_rn 127
 // cycles dependent, ~2 divisions / cycle / SM at 256 threads)

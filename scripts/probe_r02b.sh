@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-3 session probe: fine-grained selection anatomy (experiment build) + baseline bench lines.
+# Round-2b session probe: fine-grained selection anatomy (experiment build) + baseline bench lines.
 o=gpurun_out/probe; mkdir -p $o
 export SIMPLEX_EXPERIMENT_LIB=$PWD/build/libsimplex_exp.so
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $o/smi.txt
