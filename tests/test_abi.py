@@ -101,6 +101,10 @@ def test_argument_errors_before_any_device_work():
     h = C.c_void_p()
     assert sx.lib().simplex_create(C.byref(h), 2, 2, None, None, None, None) == sx.E_ARG
     assert sx.lib().simplex_destroy(None) == sx.OK
+    # simplex_solve_lp: NULL handle / NULL inputs are argument errors (no device work)
+    obj, piv, st = C.c_double(), C.c_int64(), C.c_int()
+    assert sx.lib().simplex_solve_lp(None, A.ctypes.data, b.ctypes.data, c.ctypes.data, None, None,
+                                     C.byref(obj), C.byref(piv), C.byref(st)) == sx.E_ARG
     bad = sx.default_options()
     bad.struct_size = 7
     assert sx.lib().simplex_create(C.byref(h), 2, 2, A.ctypes.data, b.ctypes.data, c.ctypes.data,
