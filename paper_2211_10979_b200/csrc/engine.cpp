@@ -1004,11 +1004,13 @@ simplex_err simplex_s::solve_lp_small(const double* A, const double* b, const do
     if (hb) db = d_stage + m * n;
     if (hc) dc = d_stage + m * n + m;
   }
-  const sx::SmallLP io{dA, db, dc, n, d_x, d_y, d_res};
+  // outputs on this device are written by the kernel itself (no copies)
+  const bool dx = x && on_device(x, device), dy = y && on_device(y, device);
+  const sx::SmallLP io{dA, db, dc, n, dx ? x : d_x, dy ? y : d_y, d_res};
   CK(sx::launch_solve_small(slabs[0].v, LLONG_MAX, opt.tol_opt, opt.tol_piv, stream, io));
   ++kernel_launches;
-  if (x) CK(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDefault, stream));
-  if (y) CK(cudaMemcpyAsync(y, d_y, sizeof(double) * m, cudaMemcpyDefault, stream));
+  if (x && !dx) CK(cudaMemcpyAsync(x, d_x, sizeof(double) * n, cudaMemcpyDefault, stream));
+  if (y && !dy) CK(cudaMemcpyAsync(y, d_y, sizeof(double) * m, cudaMemcpyDefault, stream));
   CK(cudaMemcpyAsync(h_res, d_res, sizeof(double) * 4, cudaMemcpyDeviceToHost, stream));
   CK(cudaStreamSynchronize(stream));
   slot_ready = false;

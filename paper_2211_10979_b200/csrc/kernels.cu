@@ -2146,7 +2146,7 @@ __global__ void __launch_bounds__(NT, 1) k_solve_small(SlabView s, long long sto
       const double a = T[(size_t)i * cols + k];
       if (a > tol_piv) q = cand_min(q, ratio_cand(rule, __ddiv_rn(T[(size_t)i * cols + rhs], a), i, basis[i - 1]));
     }
-    q = warp_min(q);
+    if (32 * wid + 1 <= m) q = warp_min(q);           // (warps without rows keep "none")
     if (lane == 0) slot[wid] = q;
     __syncthreads();                                                      // barrier 1
     q = warp_min(lane < NW ? slot[lane] : cand_none());
