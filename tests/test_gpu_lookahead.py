@@ -281,3 +281,22 @@ def test_selection_kernel_choice(sx, m, n, want, ov):
     with sx.Simplex(A, b, c, max_pivots=120, overlap=ov) as s:
         assert s.stats().path == want
     assert_same(gpu_solve(sx, A, b, c, max_pivots=120, lookahead=0, overlap=ov), o)
+
+
+def test_look2_two_columns_iterate_windows(sx, ov):
+    """k_look2's two-column configuration (pitch > 4096 doubles) stopped inside blocks: every window
+    end leaves a partial bank whose hand-off the next launch chains first (spre < 16)."""
+    A, b, c = lpgen.dense_lp(2600, 2000, 11)             # pitch 4608: two own columns per thread
+    with sx.Simplex(A, b, c, overlap=ov) as s:
+        assert s.stats().path == 3
+        done_total = 0
+        for step in (5, 23, 37, 16, 19):
+            done, st = s.iterate(step)
+            done_total += done
+            o = oracle.solve(A, b, c, stop_after=done_total, keep_tableau=True)
+            T, _ = s.tableau()
+            k, r = s.trace()
+            assert np.array_equal(k, o.trace_k) and np.array_equal(r, o.trace_r), done_total
+            assert np.array_equal(T, o.T), done_total
+            if st != sx.RUNNING:
+                break
