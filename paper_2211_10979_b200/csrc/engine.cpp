@@ -1520,6 +1520,6 @@ simplex_err simplex_partition(int64_t total_cols, int64_t nparts, int64_t part, 
   return SIMPLEX_OK;
 }
 
-const char* simplex_version(void) { return "libsimplex 0.2.0 (sm_100a, dense full-tableau simplex)"; }
+const char* simplex_version(void) { return "libsimplex 0.3.0 (sm_100a, dense full-tableau simplex)"; }
 
 }  // extern "C"
